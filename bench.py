@@ -1,0 +1,388 @@
+#!/usr/bin/env python
+"""BitSnap B200 codec benchmark (driver contract: one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1], "C1"): one flat bf16 tensor of 2^30
+elements, base ~ N(0, 0.02) in bf16, current = base with k = round(p*n)
+distinct uniformly-random elements moved by +-1 ulp (p = 1 % by default).
+A step = bitmask encode of (base, current) followed by the decode of that
+record back onto base, i.e. the save + restore pair of one delta checkpoint.
+
+  value  = whole-job algorithmic GB/s, inputs resident in HBM
+           (encode 4n + n/8 + 2n_c, decode n/8 + 2n_c + 4n bytes)
+  e2e    = the same through pinned host buffers: H2D of the inputs and D2H of
+           the encoded record / decoded tensor inside the timed region
+  --impl reference : the reference algorithm (CPU oracle port, numpy, all host
+           cores) on a bounded sample of the same workload.
+
+Multi-GPU (torchrun): every rank encodes/decodes its own 2^30 shard (weak
+scaling); the shard planner's NCCL all-gather of the per-rank size table is
+part of every step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "bitmask delta encode+decode throughput (C1: 2^30 bf16, p changed)"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--log2n", type=int, default=30)
+    ap.add_argument("--p", type=float, default=0.01)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-elems-per-core", type=int, default=1 << 23)
+    return ap.parse_args()
+
+
+def algo_bytes(n: int, n_c: int) -> tuple[int, int]:
+    mask = (n + 7) // 8
+    return 4 * n + mask + 2 * n_c, mask + 2 * n_c + 4 * n
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu
+    capture (profiles/ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling during the timed region
+# ---------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        time.sleep(0.25)
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9 and parts[1].isdigit():
+                    rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        sm = sorted(int(r[1]) for r in rows)
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for name, v in zip(names, r[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": int(rows[0][2]),
+                "samples": len(rows), "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the reference algorithm (oracle port) on all host cores
+# ---------------------------------------------------------------------------
+def _cpu_worker(args):
+    seed, n, p, barrier = args
+    import numpy as np
+    from oracle import bitsnap_oracle as O
+    rng = np.random.default_rng(seed)
+    f = (rng.standard_normal(n, dtype=np.float32) * 0.02).view(np.uint32).astype(np.uint64)
+    base = ((f + ((f >> 16) & 1) + 0x7FFF) >> 16).astype(np.uint16)
+    cur = base.copy()
+    k = int(round(p * n))
+    idx = rng.choice(n, k, replace=False)
+    cur[idx] += 1
+    barrier.wait()
+    t0 = time.perf_counter()
+    mask, payload, n_c = O.delta_encode(base, cur)
+    out = O.delta_decode(base, mask, payload, n, n_c)
+    dt = time.perf_counter() - t0
+    assert out[idx[0]] == cur[idx[0]]
+    e, d = algo_bytes(n, n_c)
+    return e + d, dt, t0
+
+
+def cpu_baseline(p: float, per_core: int, cores: int | None = None, reps: int = 1):
+    import multiprocessing as mp
+    cores = cores or len(os.sched_getaffinity(0))
+    ctx = mp.get_context("fork")
+    best = None
+    with ctx.Manager() as mgr:
+        for r in range(reps):
+            barrier = mgr.Barrier(cores)
+            with ctx.Pool(cores) as pool:
+                res = pool.map(_cpu_worker, [(1000 * r + i, per_core, p, barrier)
+                                             for i in range(cores)])
+            total = sum(x[0] for x in res)
+            start = min(x[2] for x in res)
+            end = max(x[2] + x[1] for x in res)
+            gbs = total / (end - start) / 1e9
+            best = gbs if best is None else max(best, gbs)
+    try:
+        model = [l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo")
+                 if l.startswith("model name")][0]
+    except Exception:
+        model = "unknown"
+    return {"value": round(best, 3), "unit": "GB/s", "cores": cores,
+            "kind": "port",
+            "sample": f"{cores} x {per_core} bf16 elements (one per core), p={p}, "
+                      f"numpy oracle encode+decode, best of {reps}; cpu: {model}"}
+
+
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return
+    per_core = args.cpu_elems_per_core
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_baseline(args.p, per_core, reps=1)
+        if i >= args.warmup:
+            vals.append(r["value"])
+    v = sorted(vals)[len(vals) // 2]
+    line = {"metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "impl": "reference",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u16", "data": "synthetic",
+            "config": {"workload": "C1 bitmask encode+decode (bounded CPU sample)",
+                       "n": r["sample"], "p": args.p},
+            "cpu_baseline": {**r, "value": v},
+            "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+def make_c1(n: int, p: float, seed: int, dev):
+    """Seeded C1 generator: exactly k = round(p n) changes."""
+    import torch
+    g = torch.Generator(device=dev).manual_seed(seed)
+    base = (torch.randn(n, device=dev, generator=g) * 0.02).to(torch.bfloat16)
+    base = base.view(torch.int16)
+    k = int(round(p * n))
+    idx = torch.randperm(n, device=dev, generator=g)[:k]
+    sgn = torch.randint(0, 2, (k,), device=dev, generator=g, dtype=torch.int32) * 2 - 1
+    vals = base[idx].to(torch.int32) & 0xFFFF
+    sgn = torch.where((vals & 0x7FFF) == 0, torch.ones_like(sgn), sgn)
+    cur = base.clone()
+    v = (vals + sgn) & 0xFFFF
+    cur[idx] = torch.where(v > 32767, v - 65536, v).to(torch.int16)
+    del idx, sgn, vals
+    torch.cuda.synchronize(dev)
+    return base, cur, k
+
+
+def run_b200(args, rank: int, world: int, local_rank: int):
+    import torch
+    import torch.distributed as dist
+    from paper_2511_12376_b200 import bitmask as B
+    from paper_2511_12376_b200 import _runtime as rt
+    from paper_2511_12376_b200 import planner
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    n = 1 << args.log2n
+    base, cur, k = make_c1(n, args.p, args.seed + rank, dev)
+    mask = torch.empty((n + 7) // 8, dtype=torch.uint8, device=dev)
+    payload = torch.empty(n, dtype=torch.int16, device=dev)
+    out = torch.empty_like(base)
+    st = rt.new_status(dev, 2)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(timing=None):
+        if timing:
+            timing[0].record(stream)
+        B.encode_delta_async(base, cur, mask, payload, st[0])
+        if timing:
+            timing[1].record(stream)
+        (n_c, flags), = rt.read_status(st[0:1])
+        if world > 1:
+            planner.exchange_sizes([(0, 1, n_c, (n + 7) // 8 + 2 * n_c)], world)
+        if timing:
+            timing[2].record(stream)
+        B.decode_delta_async(base, mask, payload[:n_c], n_c, out, st[1])
+        if timing:
+            timing[3].record(stream)
+        return n_c, flags
+
+    for _ in range(args.warmup):
+        n_c, flags = step()
+    assert n_c == k and flags == 0, (n_c, k, flags)
+    torch.cuda.synchronize(dev)
+    # correctness of the timed configuration: decode(encode(cur)) == cur
+    assert torch.equal(out, cur)
+
+    clocks = Clocks(local_rank)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clocks.start()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for i in range(args.steps):
+        step(evs[i])
+    t_end.record(stream)
+    torch.cuda.synchronize(dev)
+    clk = clocks.stop()
+    ms = t_start.elapsed_time(t_end) / args.steps
+    enc_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
+    dec_ms = sum(e[2].elapsed_time(e[3]) for e in evs) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+
+    eb, db = algo_bytes(n, k)
+    value = world * (eb + db) / (ms * 1e-3) / 1e9
+
+    # ---------------- e2e through pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, base, cur, k, dev, world)
+
+    if rank != 0:
+        return
+    hbm, peak_kind = peaks()
+    dom = "delta_encode" if enc_ms >= dec_ms else "delta_decode"
+    dom_ms = max(enc_ms, dec_ms)
+    dom_bytes = eb if dom == "delta_encode" else db
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    traffic = ncu_traffic().get(dom)
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u16", "data": "synthetic",
+        "config": {"workload": "C1", "n_per_gpu": n, "p": args.p, "n_c": k,
+                   "dtype": "bf16 (raw u16 patterns)", "parallelism": f"shard x{world}",
+                   "l2": "inputs 4 GiB >> 126 MB L2 (no flush needed)"},
+        "ops": {"encode_gbs": round(eb / (enc_ms * 1e-3) / 1e9, 1),
+                "decode_gbs": round(db / (dec_ms * 1e-3) / 1e9, 1),
+                "encode_ms": round(enc_ms, 4), "decode_ms": round(dec_ms, 4),
+                "compression_ratio": round(2 * n / (B.delta_size_bytes(n, k) + 1), 4)},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
+                     "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": round(achieved / hbm, 4),
+                     "algorithmic_bytes": dom_bytes,
+                     "traffic": traffic},
+        "gpu_launches": 2 * args.steps,
+        "clocks": clk,
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(args.p, args.cpu_elems_per_core)
+    print(json.dumps(line), flush=True)
+
+
+def run_e2e(args, base, cur, k, dev, world):
+    """Encode + decode through pinned host memory (H2D inputs, D2H results)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2511_12376_b200 import hostpath
+
+    n = base.numel()
+    base_h = base.cpu().pin_memory()
+    cur_h = cur.cpu().pin_memory()
+    codec = hostpath.HostDeltaCodec(dev, n)
+    for _ in range(max(1, args.warmup)):
+        rec = codec.encode(base_h, cur_h)
+        out_h = codec.decode(base_h, rec)
+    assert rec.n_c == k and torch.equal(out_h, cur_h)
+    steps = max(2, args.steps // 2)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        rec = codec.encode(base_h, cur_h)
+        out_h = codec.decode(base_h, rec)
+    torch.cuda.synchronize(dev)
+    dt = (time.perf_counter() - t0) / steps
+    if world > 1:
+        t = torch.tensor([dt], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    eb, db = algo_bytes(n, k)
+    mask = (n + 7) // 8
+    return {"value": round(world * (eb + db) / dt / 1e9, 2), "unit": "GB/s",
+            "h2d_bytes_per_step": 4 * n + mask + 2 * k,
+            "d2h_bytes_per_step": mask + 2 * k + 2 * n,
+            "ms_per_step": round(dt * 1e3, 3), "steps": steps,
+            "path": "hostpath.HostDeltaCodec (pinned host in/out, chunked streams)"}
+
+
+def main():
+    args = parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_b200(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

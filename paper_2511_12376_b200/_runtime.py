@@ -1,0 +1,102 @@
+"""Device plumbing around the C-ABI: workspaces, status blocks, staging.
+
+PyTorch is used only for device memory, pinned host memory and streams; all
+codec arithmetic runs in `_bsnp.so`.
+"""
+
+from __future__ import annotations
+
+import threading
+
+import numpy as np
+import torch
+
+from . import _lib
+
+_tls = threading.local()
+
+
+def device_of(t: torch.Tensor | None = None) -> torch.device:
+    if t is not None and t.is_cuda:
+        return t.device
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2511_12376_b200 needs a CUDA device (no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_ptr(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _cache() -> dict:
+    c = getattr(_tls, "cache", None)
+    if c is None:
+        c = _tls.cache = {}
+    return c
+
+
+def workspace(device: torch.device, nbytes: int, slot: str = "ws") -> torch.Tensor:
+    """Growable per-(thread, device, stream, slot) scratch buffer.
+
+    Work on one stream is ordered, so reuse across calls is safe; distinct
+    streams get distinct buffers.
+    """
+    key = (slot, device.index, stream_ptr(device))
+    c = _cache()
+    buf = c.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(int(nbytes * 1.25), 256), dtype=torch.uint8, device=device)
+        c[key] = buf
+    return buf
+
+
+def new_status(device: torch.device, count: int = 1) -> torch.Tensor:
+    """`count` bsnp_status blocks (16 B each) as an int64 [count, 2] tensor."""
+    return torch.empty((count, 2), dtype=torch.int64, device=device)
+
+
+def read_status(st: torch.Tensor):
+    """-> list of (count, err_flags) after a device sync on the status copy."""
+    h = st.cpu().numpy()
+    return [(int(r[0]) & 0xFFFFFFFFFFFFFFFF, int(r[1]) & 0xFFFFFFFF) for r in h]
+
+
+def pinned(nbytes: int, slot: str = "pin") -> torch.Tensor:
+    key = ("pin", slot)
+    c = _cache()
+    buf = c.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 4096), dtype=torch.uint8, pin_memory=True)
+        c[key] = buf
+    return buf[:nbytes]
+
+
+def h2d_bytes(data, device: torch.device, dtype: torch.dtype = torch.uint8) -> torch.Tensor:
+    """Host bytes -> new device tensor (via pinned staging)."""
+    raw = np.frombuffer(data, dtype=np.uint8)
+    out = torch.empty(raw.size, dtype=torch.uint8, device=device)
+    if raw.size:
+        stage = pinned(raw.size, "h2d")
+        stage.numpy()[:] = raw
+        out.copy_(stage, non_blocking=True)
+        torch.cuda.current_stream(device).synchronize()  # staging buffer is reused
+    return out.view(dtype)
+
+
+def d2h_bytes(t: torch.Tensor) -> bytes:
+    """Device tensor -> bytes (via pinned staging)."""
+    flat = t.reshape(-1).view(torch.uint8)
+    if flat.numel() == 0:
+        return b""
+    stage = pinned(flat.numel(), "d2h")
+    stage.copy_(flat, non_blocking=True)
+    torch.cuda.current_stream(t.device).synchronize()
+    return stage.numpy().tobytes()
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def lib():
+    return _lib.load()

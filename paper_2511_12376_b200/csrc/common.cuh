@@ -1,0 +1,152 @@
+// Shared device helpers for the BitSnap sm_100a kernels.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/bitsnap_b200.h"
+
+namespace bsnp {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// ---------------------------------------------------------------------------
+// Memory access helpers
+// ---------------------------------------------------------------------------
+
+// Streaming 128-bit load: read-only path, no L1 allocation, 256B L2 prefetch.
+__device__ __forceinline__ uint4 ld_stream_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ float4 ld_stream_f4(const float* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// Streaming 128-bit store (evict-first in L2: outputs are not re-read).
+__device__ __forceinline__ void st_stream_v4(void* p, uint4 v) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Decoupled look-back over per-tile status words (single-pass prefix scan).
+// Word layout: [63:62] flag (0 = not ready, 1 = tile aggregate, 2 = inclusive
+// prefix), [61:0] value.  Flag and value live in one 64-bit word, so a
+// relaxed single-copy-atomic store publishes both at once.
+// Must be called by all 32 lanes of ONE warp; returns the exclusive prefix
+// of `tile` (valid on every lane) and publishes tile's inclusive prefix.
+// Forward progress: tiles are claimed in increasing order by resident CTAs
+// (atomic ticket), so every predecessor is running or done.
+// ---------------------------------------------------------------------------
+constexpr uint64_t kFlagAgg = 1ull << 62;
+constexpr uint64_t kFlagInc = 2ull << 62;
+constexpr uint64_t kValMask = (1ull << 62) - 1;
+
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(kFull, v, d);
+  return v;
+}
+
+__device__ __forceinline__ uint64_t lookback_exclusive(uint64_t* status, uint64_t tile,
+                                                       uint64_t aggregate, int lane) {
+  if (tile == 0) {
+    if (lane == 0) st_relaxed_u64(status, kFlagInc | aggregate);
+    return 0;
+  }
+  if (lane == 0) st_relaxed_u64(status + tile, kFlagAgg | aggregate);
+  uint64_t excl = 0;
+  int64_t top = (int64_t)tile - 1;
+  while (true) {
+    const int64_t idx = top - lane;
+    uint64_t s;
+    uint32_t inc, relevant;
+    while (true) {
+      s = idx >= 0 ? ld_relaxed_u64(status + idx) : kFlagInc;
+      const uint32_t flag = (uint32_t)(s >> 62);
+      const uint32_t bad = __ballot_sync(kFull, flag == 0);
+      inc = __ballot_sync(kFull, flag == 2);
+      const int first = inc ? __ffs(inc) - 1 : 31;
+      relevant = first == 31 ? kFull : ((2u << first) - 1u);
+      if (!(bad & relevant)) break;
+      __nanosleep(32);
+    }
+    const uint64_t v = (relevant >> lane) & 1u ? (s & kValMask) : 0;
+    excl += warp_sum_u64(v);
+    if (inc) break;
+    top -= 32;
+  }
+  if (lane == 0) st_relaxed_u64(status + tile, kFlagInc | (excl + aggregate));
+  return excl;
+}
+
+// Warp inclusive scan of packed 16-bit counters (4 lanes of a u64).
+__device__ __forceinline__ uint64_t warp_inclusive_scan_u64(uint64_t v, int lane) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint64_t o = __shfl_up_sync(kFull, v, d);
+    if (lane >= d) v += o;
+  }
+  return v;
+}
+
+__device__ __forceinline__ uint32_t warp_inclusive_scan_u32(uint32_t v, int lane) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t o = __shfl_up_sync(kFull, v, d);
+    if (lane >= d) v += o;
+  }
+  return v;
+}
+
+// Halfword k (0..7) of an 8 x u16 vector held in a uint4, k dynamic, no local memory.
+__device__ __forceinline__ uint32_t u16_lane(const uint4& v, uint32_t k) {
+  const uint32_t lo = (k & 2) ? v.y : v.x;
+  const uint32_t hi = (k & 2) ? v.w : v.z;
+  const uint32_t w = (k & 4) ? hi : lo;
+  return (k & 1) ? (w >> 16) : (w & 0xffffu);
+}
+
+__device__ __forceinline__ void set_u16_lane(uint4& v, uint32_t k, uint32_t val) {
+  const uint32_t sh = (k & 1) * 16;
+  const uint32_t keep = ~(0xffffu << sh), ins = (val & 0xffffu) << sh;
+  const uint32_t w = k >> 1;
+  if (w == 0) v.x = (v.x & keep) | ins;
+  else if (w == 1) v.y = (v.y & keep) | ins;
+  else if (w == 2) v.z = (v.z & keep) | ins;
+  else v.w = (v.w & keep) | ins;
+}
+
+// 8-bit change mask of two 8 x u16 vectors: bit k = halfword k differs.
+__device__ __forceinline__ uint32_t diff8(const uint4& a, const uint4& b) {
+  const uint32_t d0 = __vcmpne2(a.x, b.x), d1 = __vcmpne2(a.y, b.y);
+  const uint32_t d2 = __vcmpne2(a.z, b.z), d3 = __vcmpne2(a.w, b.w);
+  // each dK holds 0xffff per differing halfword; gather one bit per halfword
+  const uint32_t p01 = __byte_perm(d0, d1, 0x6420);  // bytes: d0.lo d0.hi d1.lo d1.hi
+  const uint32_t p23 = __byte_perm(d2, d3, 0x6420);
+  const uint32_t lo = ((p01 & 0x01010101u) * 0x01020408u) >> 24;
+  const uint32_t hi = ((p23 & 0x01010101u) * 0x01020408u) >> 24;
+  return (lo & 0xfu) | ((hi & 0xfu) << 4);
+}
+
+}  // namespace bsnp
