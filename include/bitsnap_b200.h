@@ -62,8 +62,11 @@ int bsnp_device_sm_count(void);
  * Bitmask delta codec
  * ---------------------------------------------------------------------- */
 
-/* Workspace for one encode or decode call over n elements. */
-size_t bsnp_delta_ws_bytes(uint64_t n);
+/* Workspace of one encode call over n elements (tile status words plus an
+ * L2-resident payload staging area of 2*n bytes rounded up to whole tiles). */
+size_t bsnp_delta_encode_ws_bytes(uint64_t n);
+/* Workspace of one decode call over n elements (about n/1024 bytes). */
+size_t bsnp_delta_decode_ws_bytes(uint64_t n);
 
 /*
  * Replaces bitmask.encode_delta (bitmask.py:94-111).

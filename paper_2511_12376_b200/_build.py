@@ -47,10 +47,10 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str = OUT, extra=()) -> str:
+    if out == OUT and not extra and not force and up_to_date():
         return OUT
-    cmd = [nvcc_path(), *ARCH, *FLAGS, "-o", OUT + ".tmp", *sources()]
+    cmd = [nvcc_path(), *ARCH, *FLAGS, *extra, "-o", out + ".tmp", *sources()]
     if verbose:
         print(" ".join(cmd), flush=True)
     res = subprocess.run(cmd, capture_output=True, text=True)
@@ -59,8 +59,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed building _bsnp.so")
     if verbose and (res.stdout or res.stderr):
         sys.stderr.write(res.stdout + res.stderr)
-    os.replace(OUT + ".tmp", OUT)
-    return OUT
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":

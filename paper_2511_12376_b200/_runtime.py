@@ -45,7 +45,8 @@ def workspace(device: torch.device, nbytes: int, slot: str = "ws") -> torch.Tens
     c = _cache()
     buf = c.get(key)
     if buf is None or buf.numel() < nbytes:
-        buf = torch.empty(max(int(nbytes * 1.25), 256), dtype=torch.uint8, device=device)
+        buf = torch.empty((max(int(nbytes * 1.25), 256) + 255) // 256 * 256, dtype=torch.uint8,
+                          device=device)
         c[key] = buf
     return buf
 

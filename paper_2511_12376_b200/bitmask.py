@@ -100,8 +100,8 @@ def encode_delta_async(base: torch.Tensor, target: torch.Tensor, mask: torch.Ten
     b, c = _as_i16(base), _as_i16(target)
     n = b.numel()
     dev = b.device
-    ws_n = rt.lib().bsnp_delta_ws_bytes(n)
-    ws = rt.workspace(dev, ws_n)
+    ws_n = rt.lib().bsnp_delta_encode_ws_bytes(n)
+    ws = rt.workspace(dev, ws_n, "enc")
     _lib.check(rt.lib().bsnp_delta_encode(
         b.data_ptr(), c.data_ptr(), n, mask.data_ptr(), payload.data_ptr(),
         payload.numel(), status.data_ptr(), ws.data_ptr(), ws.numel(),
@@ -132,8 +132,8 @@ def decode_delta_async(base: torch.Tensor, mask: torch.Tensor, payload: torch.Te
     o = out.reshape(-1).view(torch.int16)
     n = b.numel()
     dev = b.device
-    ws_n = rt.lib().bsnp_delta_ws_bytes(n)
-    ws = rt.workspace(dev, ws_n)
+    ws_n = rt.lib().bsnp_delta_decode_ws_bytes(n)
+    ws = rt.workspace(dev, ws_n, "dec")
     _lib.check(rt.lib().bsnp_delta_decode(
         b.data_ptr(), mask.data_ptr(), payload.data_ptr() if payload.numel() else None,
         n, n_c, o.data_ptr(), status.data_ptr(), ws.data_ptr(), ws.numel(),

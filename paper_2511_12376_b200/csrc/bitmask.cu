@@ -13,6 +13,8 @@
 // Payload positions (ascending element order, bitmask.py:103) come from a
 // block scan of per-group popcounts (packed 4 x 16-bit in a u64) plus a
 // decoupled look-back across tiles (common.cuh), so the data is read once.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "runtime.cuh"
 
@@ -146,134 +148,566 @@ __global__ void __launch_bounds__(kThreads)
   if (overflow) atomicOr(&st->err_flags, BSNP_ERR_PAYLOAD_CAP);
 }
 
-// ------------------------------------------------------------------ decode
-// Mask pre-check for in-place decode: popcount of mask[:n] and padding bits.
-__global__ void __launch_bounds__(256)
-    delta_mask_check_kernel(const uint8_t* __restrict__ mask, uint64_t n,
-                            bsnp_status* __restrict__ st) {
-  const uint64_t nbytes = (n + 7) / 8;
-  uint64_t local = 0;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nbytes;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t b = mask[i];
-    const uint64_t e0 = i * 8;
-    if (e0 + 8 > n) {
-      const uint32_t valid = (uint32_t)(n - e0);
-      if (b >> valid) atomicOr(&st->err_flags, BSNP_ERR_PADDING);
-      b &= (1u << valid) - 1u;
-    }
-    local += __popc(b);
-  }
-  local = warp_sum_u64(local);
-  if ((threadIdx.x & 31) == 0 && local) atomicAdd((unsigned long long*)&st->count, local);
-}
+// ===========================================================================
+// TMA-pipelined persistent kernels (16B-aligned operands, full tiles).
+// Thread 0 claims tile tickets and issues cp.async.bulk copies of the
+// operands into shared-memory stages that complete on mbarriers, so loads of
+// later tiles are in flight while earlier tiles are scanned and written.
+// ===========================================================================
+constexpr uint32_t kTileBytes = kTile * 2;                    // 16 KiB per u16 operand
+constexpr uint32_t kMaskBytes = kTile / 8;                    // 1 KiB
+constexpr uint32_t kEncStage = 2 * kTileBytes;                // base + cur
+constexpr uint32_t kDecPayloadCap = kTileBytes + 32;          // aligned superset of a slice
+constexpr uint32_t kDecStage = kTileBytes + kMaskBytes + kDecPayloadCap + 96;  // 128B multiple
+static_assert(kDecStage % 128 == 0, "stage alignment");
 
-__global__ void delta_check_finish_kernel(bsnp_status* st, uint64_t n_c) {
-  if (st->count != n_c) st->err_flags |= BSNP_ERR_POPCOUNT;
-}
-
-template <bool kAligned, bool kInPlace>
-__global__ void __launch_bounds__(kThreads)
-    delta_decode_kernel(const uint16_t* base, const uint8_t* __restrict__ mask,
-                        const uint16_t* __restrict__ payload, uint64_t n, uint64_t n_c,
-                        uint16_t* out, bsnp_status* __restrict__ st,
-                        uint32_t* __restrict__ ticket, uint64_t* __restrict__ tile_status,
-                        uint64_t ntiles) {
-  __shared__ uint64_t s_warp[kWarps];
-  __shared__ uint32_t s_off[kVec][kWarps];
-  __shared__ uint64_t s_prefix[2];
-  __shared__ uint32_t s_tile;
-
-  const int tid = threadIdx.x;
-  if (kInPlace) {
-    // the pre-check kernel validated the whole mask; never touch base on error
-    if (*(volatile uint32_t*)&st->err_flags) return;
-  }
-  if (tid == 0) s_tile = atomicAdd(ticket, 1u);
-  __syncthreads();
-  const uint64_t tile = s_tile;
-  const uint64_t t0 = tile * kTile;
-  const bool full = t0 + kTile <= n;
-  const uint64_t g0 = t0 / 8;
-
-  uint32_t bits[kVec], cnt[kVec];
-  bool pad_err = false;
+// Packed-count scan of one tile inside the CTA (no look-back): returns this
+// thread's offsets of its kVec groups relative to the tile start, and the
+// tile total.  Two barriers.
+__device__ __forceinline__ uint32_t tile_local_scan(const uint32_t (&cnt)[kVec],
+                                                    uint32_t (&off)[kVec], uint64_t* s_warp,
+                                                    uint32_t (*s_off)[kWarps]) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint64_t packed = 0;
 #pragma unroll
-  for (int j = 0; j < kVec; ++j) {
-    const uint64_t g = g0 + j * kThreads + tid;
-    uint32_t b = 0;
-    if (full) {
-      b = __ldg(mask + g);
-    } else if (g * 8 < n) {
-      b = __ldg(mask + g);
-      if (g * 8 + 8 > n) {
-        const uint32_t valid = (uint32_t)(n - g * 8);
-        pad_err |= (b >> valid) != 0;
-        b &= (1u << valid) - 1u;
+  for (int j = 0; j < kVec; ++j) packed |= (uint64_t)cnt[j] << (16 * j);
+  const uint64_t inc = warp_inclusive_scan_u64(packed, lane);
+  if (lane == 31) s_warp[warp] = inc;
+  __syncthreads();
+  uint32_t total = 0;
+  if (warp == 0) {
+    const int j = lane / kWarps, w = lane % kWarps;
+    const uint32_t v = (uint32_t)(s_warp[w] >> (16 * j)) & 0xffffu;
+    const uint32_t x = warp_inclusive_scan_u32(v, lane);
+    s_off[j][w] = x - v;
+    total = __shfl_sync(kFull, x, 31);
+  }
+  __syncthreads();
+  const uint64_t ex = inc - packed;
+#pragma unroll
+  for (int j = 0; j < kVec; ++j)
+    off[j] = s_off[j][warp] + ((uint32_t)(ex >> (16 * j)) & 0xffffu);
+  return total;
+}
+
+// Warp-specialized single-pass encode.  Roles per CTA:
+//   workers (warps 0..7): per tile (claimed by ticket, operands streamed into
+//       a shared-memory stage by cp.async.bulk), read the stage into registers
+//       and release it at once (refill = bulk copies of the next claimed
+//       tile), scan the change bits inside the CTA, publish the tile aggregate
+//       for the decoupled look-back, write the mask bytes and stage the tile's
+//       compacted payload in its own scratch slot (scratch + tile*kTile).
+//       Workers never wait for a look-back.
+//   look-back warps (8..8+kLB-1): record q of the CTA (ring of kRing) is served
+//       by warp 8 + q % kLB: decoupled look-back for the tile's exclusive
+//       prefix, then - once the workers signalled the slot staged - move the
+//       slot to payload[prefix...] and discard the slot's L2 lines so the
+//       staging never reaches DRAM.
+// mbarriers: full[s] (TMA bytes), rec_full[r]/rec_empty[r] (workers <->
+// look-back warp), staged[r] (8 worker warps -> look-back warp).
+#ifndef BSNP_LB_WIDTH
+#define BSNP_LB_WIDTH 4  // look-back predecessors per lane per round trip
+#endif
+#ifndef BSNP_KLB
+#define BSNP_KLB 1
+#endif
+constexpr int kLB = BSNP_KLB;  // look-back warps per CTA
+constexpr int kRing = 16;
+static_assert(kRing % kLB == 0, "ring slots map to look-back warps");
+constexpr int kEncThreads = kThreads + 32 * kLB;
+constexpr int kEncStagesWS = 2;
+
+__device__ __forceinline__ void mbar_arrive_release(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void discard_l2_line(const void* p) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+
+__global__ void __launch_bounds__(kEncThreads)
+    delta_encode_ws_kernel(const uint16_t* __restrict__ base, const uint16_t* __restrict__ cur,
+                           uint64_t n, uint8_t* __restrict__ mask,
+                           uint16_t* __restrict__ payload, uint64_t payload_cap,
+                           uint16_t* __restrict__ scratch, bsnp_status* __restrict__ st,
+                           uint32_t* __restrict__ ticket, uint64_t* __restrict__ tile_status,
+                           uint64_t ntiles) {
+  constexpr int kStages = kEncStagesWS;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint64_t full_bar[kStages];
+  __shared__ uint64_t rec_full[kRing], rec_empty[kRing], staged[kRing];
+  __shared__ uint32_t s_tile[kStages];
+  __shared__ uint32_t r_tile[kRing], r_count[kRing];
+  __shared__ uint64_t s_warp[2][kWarps];
+  __shared__ uint32_t s_off[2][kVec][kWarps];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t nfull = n / kTile;
+  uint64_t pol = 0;
+  auto refill = [&](int s, uint32_t t) {  // worker thread 0 only
+    s_tile[s] = t;
+    if (t < nfull) {
+      uint8_t* dst = smem + (size_t)s * kEncStage;
+      mbar_arrive_expect_tx(&full_bar[s], kEncStage);
+      bulk_g2s(dst, base + (uint64_t)t * kTile, kTileBytes, &full_bar[s], pol);
+      bulk_g2s(dst + kTileBytes, cur + (uint64_t)t * kTile, kTileBytes, &full_bar[s], pol);
+    }
+  };
+  // ring producer (worker thread 0): record q -> slot q % kRing
+  auto push_record = [&](uint32_t q, uint32_t tile, uint32_t count) {
+    const int r = q % kRing;
+    if (q >= kRing) mbar_wait(&rec_empty[r], ((q / kRing) - 1) & 1u);
+    r_tile[r] = tile;
+    r_count[r] = count;
+    mbar_arrive_release(&rec_full[r]);
+  };
+  if (tid == 0) {
+    pol = policy_evict_first();
+    for (int s = 0; s < kStages; ++s) mbar_init(&full_bar[s], 1);
+    for (int r = 0; r < kRing; ++r) {
+      mbar_init(&rec_full[r], 1);
+      mbar_init(&rec_empty[r], 1);
+      mbar_init(&staged[r], kWarps);
+    }
+    fence_mbar_init();
+    for (int s = 0; s < kStages; ++s) refill(s, atomicAdd(ticket, 1u));
+  }
+  __syncthreads();
+
+  if (warp >= kWarps) {
+    // ------------------------------------------------------ look-back warps
+    const int w = warp - kWarps;
+    for (uint32_t q = w;; q += kLB) {
+      const int r = q % kRing;
+      const uint32_t parity = (q / kRing) & 1u;
+      mbar_wait(&rec_full[r], parity);
+      const uint32_t tile = r_tile[r];
+      const uint32_t c = r_count[r];
+      if (tile >= ntiles) break;
+      const uint64_t excl = lookback_wide<BSNP_LB_WIDTH>(tile_status, tile, c, lane);
+      if (lane == 0 && tile == ntiles - 1) st->count = excl + c;
+      mbar_wait(&staged[r], parity);  // workers wrote the scratch slot
+      const uint16_t* src = scratch + (uint64_t)tile * kTile;
+      const bool overflow = excl + c > payload_cap;
+      if (!overflow) {
+        // 16-byte loads from the (16 KiB aligned) slot, 4 in flight per lane
+        uint16_t* dst = payload + excl;
+        const uint4* src4 = reinterpret_cast<const uint4*>(src);
+        const uint32_t nv = (c + 7) / 8;
+        for (uint32_t v0 = 0; v0 < nv; v0 += 4 * 32) {
+          uint4 buf[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint32_t v = v0 + u * 32 + lane;
+            if (v < nv) buf[u] = src4[v];
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint32_t v = v0 + u * 32 + lane;
+            if (v < nv) {
+              const uint32_t e0 = v * 8;
+#pragma unroll
+              for (uint32_t k = 0; k < 8; ++k)
+                if (e0 + k < c) dst[e0 + k] = (uint16_t)u16_lane(buf[u], k);
+            }
+          }
+        }
+      } else {
+        for (uint32_t i = lane; i < c; i += 32)
+          if (excl + i < payload_cap) payload[excl + i] = src[i];
+        if (lane == 0) atomicOr(&st->err_flags, BSNP_ERR_PAYLOAD_CAP);
+      }
+      __syncwarp();
+      for (uint32_t i = lane * 64; i < c; i += 32 * 64) discard_l2_line(src + i);
+      __syncwarp();
+      if (lane == 0) mbar_arrive_release(&rec_empty[r]);
+      __syncwarp();
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------ workers
+  for (uint32_t q = 0;; ++q) {
+    const int s = q % kStages;
+    const uint32_t parity = (q / kStages) & 1u;
+    const uint32_t tile = s_tile[s];
+    if (tile >= ntiles) {
+      // end of work: poison one record per look-back warp so each exits
+      if (tid == 0)
+        for (int k = 0; k < kLB; ++k) push_record(q + k, 0xffffffffu, 0);
+      break;
+    }
+    const uint64_t t0 = (uint64_t)tile * kTile;
+    // claim the stage's next tile now; the atomic's latency overlaps the wait
+    uint32_t next_t = 0;
+    if (tid == 0) next_t = atomicAdd(ticket, 1u);
+    uint4 cv[kVec];
+    uint32_t bits[kVec], cnt[kVec];
+    if (tile < nfull) {
+      mbar_wait(&full_bar[s], parity);
+      const uint4* sb = reinterpret_cast<const uint4*>(smem + (size_t)s * kEncStage);
+      const uint4* sc = reinterpret_cast<const uint4*>(smem + (size_t)s * kEncStage + kTileBytes);
+#pragma unroll
+      for (int j = 0; j < kVec; ++j) {
+        const uint4 b = sb[j * kThreads + tid];
+        cv[j] = sc[j * kThreads + tid];
+        bits[j] = diff8(b, cv[j]);
+      }
+    } else {  // the partial last tile: bounded global loads
+#pragma unroll
+      for (int j = 0; j < kVec; ++j) {
+        const uint64_t e = t0 + (uint64_t)(j * kThreads + tid) * 8;
+        uint4 b = make_uint4(0, 0, 0, 0), c = make_uint4(0, 0, 0, 0);
+        for (uint32_t k = 0; k < 8; ++k) {
+          if (e + k < n) {
+            set_u16_lane(b, k, base[e + k]);
+            set_u16_lane(c, k, cur[e + k]);
+          }
+        }
+        cv[j] = c;
+        bits[j] = diff8(b, c);
       }
     }
-    bits[j] = b;
-    cnt[j] = __popc(b);
-  }
-  if (!kInPlace && pad_err) atomicOr(&st->err_flags, BSNP_ERR_PADDING);
-
-  uint4 bv[kVec];
-  if (!kInPlace && kAligned && full) {
 #pragma unroll
-    for (int j = 0; j < kVec; ++j)
-      bv[j] = ld_stream_v4(base + t0 + (uint64_t)(j * kThreads + tid) * 8);
-  }
-
-  TileScan sc;
-  tile_scan(cnt, tile, tile_status, sc, s_warp, s_off, s_prefix);
-  if (!kInPlace && tid == 0 && tile == ntiles - 1) {
-    const uint64_t pc = sc.prefix + sc.total;
-    st->count = pc;
-    if (pc != n_c) atomicOr(&st->err_flags, BSNP_ERR_POPCOUNT);
-  }
-
+    for (int j = 0; j < kVec; ++j) cnt[j] = __popc(bits[j]);
+    uint64_t packed = 0;
 #pragma unroll
-  for (int j = 0; j < kVec; ++j) {
-    const uint64_t e = t0 + (uint64_t)(j * kThreads + tid) * 8;
-    uint32_t b = bits[j];
-    uint64_t pos = sc.prefix + sc.off[j];
-    if (kInPlace) {
+    for (int j = 0; j < kVec; ++j) packed |= (uint64_t)cnt[j] << (16 * j);
+    const uint64_t inc = warp_inclusive_scan_u64(packed, lane);
+    const int db = q & 1;  // double-buffered scan scratch: 2 barriers per tile
+    if (lane == 31) s_warp[db][warp] = inc;
+    asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
+    // every worker holds its part of the tile in registers: release the stage
+    if (tid == 0) refill(s, next_t);
+    if (warp == 0) {
+      const int j = lane / kWarps, w = lane % kWarps;
+      const uint32_t v = (uint32_t)(s_warp[db][w] >> (16 * j)) & 0xffffu;
+      const uint32_t x = warp_inclusive_scan_u32(v, lane);
+      s_off[db][j][w] = x - v;
+      const uint32_t total = __shfl_sync(kFull, x, 31);
+      if (lane == 0) {
+        publish_aggregate(tile_status, tile, total);
+        push_record(q, tile, total);
+      }
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
+    const uint64_t ex = inc - packed;
+    const uint64_t g0 = t0 / 8;
+#pragma unroll
+    for (int j = 0; j < kVec; ++j) {
+      const uint64_t g = g0 + j * kThreads + tid;
+      if (g * 8 < n) mask[g] = (uint8_t)bits[j];
+    }
+    uint16_t* slot = scratch + t0;
+#pragma unroll
+    for (int j = 0; j < kVec; ++j) {
+      uint32_t b = bits[j];
+      uint32_t pos = s_off[db][j][warp] + ((uint32_t)(ex >> (16 * j)) & 0xffffu);
       while (b) {
         const uint32_t k = __ffs(b) - 1;
         b &= b - 1;
-        if (pos < n_c) out[e + k] = payload[pos];
-        ++pos;
+        slot[pos++] = (uint16_t)u16_lane(cv[j], k);
       }
-    } else if (kAligned && full) {
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive_release(&staged[q % kRing]);
+  }
+}
+
+// Payload offsets of every decode tile from the mask alone (n/8 bytes):
+// offsets[t] = popcount(mask[0 .. t*kTile)), offsets[ntiles] = total.  Also
+// validates padding bits and popcount == n_c (bitmask.py:128-135).  One CTA
+// per chunk of kChunkTiles tiles, chained by a decoupled look-back.
+constexpr int kChunkTiles = 32;
+
+__global__ void __launch_bounds__(kThreads)
+    delta_offsets_kernel(const uint8_t* __restrict__ mask, uint64_t n, uint64_t n_c,
+                         uint64_t* __restrict__ offsets, bsnp_status* __restrict__ st,
+                         uint32_t* __restrict__ ticket, uint64_t* __restrict__ chunk_status,
+                         uint64_t nchunks) {
+  __shared__ uint32_t s_cnt[kChunkTiles];
+  __shared__ uint32_t s_chunk;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_chunk = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const uint64_t chunk = s_chunk;
+  const uint64_t nbytes = (n + 7) / 8;
+  const uint64_t ntiles = (n + kTile - 1) / kTile;
+  bool pad = false;
+  // each warp: kChunkTiles / kWarps tiles, each tile = 1024 mask bytes = 32 lanes x 32 B
+#pragma unroll
+  for (int q = 0; q < kChunkTiles / kWarps; ++q) {
+    const int lt = warp * (kChunkTiles / kWarps) + q;
+    const uint64_t t = chunk * kChunkTiles + lt;
+    uint32_t c = 0;
+    if (t < ntiles) {
+      const uint64_t b0 = t * kMaskBytes + (uint64_t)lane * 32;
+      if (b0 + 32 <= nbytes && ((uintptr_t)(mask + b0) & 15) == 0) {
+        const uint4 a = ld_stream_v4(mask + b0), b = ld_stream_v4(mask + b0 + 16);
+        c = __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w) + __popc(b.x) +
+            __popc(b.y) + __popc(b.z) + __popc(b.w);
+        if (b0 + 32 == nbytes && (n & 7)) {  // last byte is partial
+          const uint32_t last = b.w >> 24, valid = (uint32_t)(n & 7);
+          pad |= (last >> valid) != 0;
+          c -= __popc(last >> valid);
+        }
+      } else {
+        for (uint64_t i = b0; i < b0 + 32 && i < nbytes; ++i) {
+          uint32_t v = mask[i];
+          if (i == nbytes - 1 && (n & 7)) {
+            const uint32_t valid = (uint32_t)(n & 7);
+            pad |= (v >> valid) != 0;
+            v &= (1u << valid) - 1u;
+          }
+          c += __popc(v);
+        }
+      }
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) c += __shfl_xor_sync(kFull, c, d);
+    if (lane == 0) s_cnt[lt] = c;
+  }
+  if (pad) atomicOr(&st->err_flags, BSNP_ERR_PADDING);
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t v = s_cnt[lane];  // kChunkTiles == 32
+    const uint32_t x = warp_inclusive_scan_u32(v, lane);
+    const uint32_t total = __shfl_sync(kFull, x, 31);
+    const uint64_t excl = lookback_exclusive(chunk_status, chunk, total, lane);
+    const uint64_t t = chunk * kChunkTiles + lane;
+    if (t < ntiles) offsets[t] = excl + x - v;
+    if (chunk == nchunks - 1 && lane == 0) {
+      const uint64_t pc = excl + total;
+      offsets[ntiles] = pc;
+      st->count = pc;
+      if (pc != n_c) atomicOr(&st->err_flags, BSNP_ERR_POPCOUNT);
+    }
+  }
+}
+
+template <int kStages>
+__global__ void __launch_bounds__(kThreads)
+    delta_decode_tma_kernel(const uint16_t* __restrict__ base, const uint8_t* __restrict__ mask,
+                            const uint16_t* __restrict__ payload, uint64_t n, uint64_t n_c,
+                            uint16_t* __restrict__ out, const uint64_t* __restrict__ offsets,
+                            uint32_t* __restrict__ ticket) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint64_t full_bar[kStages];
+  __shared__ uint32_t s_tile[kStages];
+  __shared__ uint32_t s_shift[kStages];   // payload element shift in smem, or ~0u: global
+  __shared__ uint64_t s_poff[kStages];
+  __shared__ uint64_t s_warp[kWarps];
+  __shared__ uint32_t s_off[kVec][kWarps];
+
+  const int tid = threadIdx.x;
+  const uint64_t nfull = n / kTile;
+  const uint64_t ntiles = (n + kTile - 1) / kTile;
+  const uintptr_t p_lo = ((uintptr_t)payload + 15) & ~(uintptr_t)15;
+  const uintptr_t p_hi = ((uintptr_t)(payload + n_c)) & ~(uintptr_t)15;
+  uint64_t pol = 0;
+  auto refill = [&](int s, uint32_t t, uint64_t off, uint64_t off_end) {  // thread 0 only
+    s_tile[s] = t;
+    if (t >= ntiles) return;
+    const uint64_t cnt = off_end - off;
+    s_poff[s] = off;
+    if (t >= nfull) {
+      s_shift[s] = ~0u;
+      return;
+    }
+    uint8_t* dst = smem + (size_t)s * kDecStage;
+    const uintptr_t a = (uintptr_t)(payload + off), b = (uintptr_t)(payload + off + cnt);
+    const uintptr_t a0 = a & ~(uintptr_t)15, a1 = (b + 15) & ~(uintptr_t)15;
+    const bool bulk_p = cnt > 0 && a0 >= p_lo && a1 <= p_hi;
+    s_shift[s] = bulk_p ? (uint32_t)((a - a0) / 2) : ~0u;
+    mbar_arrive_expect_tx(&full_bar[s], kTileBytes + kMaskBytes + (bulk_p ? (uint32_t)(a1 - a0) : 0));
+    bulk_g2s(dst, base + t * kTile, kTileBytes, &full_bar[s], pol);
+    bulk_g2s(dst + kTileBytes, mask + t * kMaskBytes, kMaskBytes, &full_bar[s], pol);
+    if (bulk_p)
+      bulk_g2s(dst + kTileBytes + kMaskBytes, (const void*)a0, (uint32_t)(a1 - a0), &full_bar[s],
+               pol);
+  };
+  if (tid == 0) {
+    pol = policy_evict_first();
+    for (int s = 0; s < kStages; ++s) mbar_init(&full_bar[s], 1);
+    fence_mbar_init();
+    for (int s = 0; s < kStages; ++s) {
+      const uint32_t t = atomicAdd(ticket, 1u);
+      refill(s, t, t < ntiles ? offsets[t] : 0, t < ntiles ? offsets[t + 1] : 0);
+    }
+  }
+  __syncthreads();
+
+  for (uint32_t it = 0;; ++it) {
+    const int s = it % kStages;
+    const uint32_t parity = (it / kStages) & 1u;
+    const uint64_t tile = s_tile[s];
+    if (tile >= ntiles) break;
+    // claim the refill tile and fetch its payload offsets off the critical path
+    uint32_t next_t = 0;
+    uint64_t next_a = 0, next_b = 0;
+    if (tid == 0) {
+      next_t = atomicAdd(ticket, 1u);
+      if (next_t < ntiles) {
+        next_a = offsets[next_t];
+        next_b = offsets[next_t + 1];
+      }
+    }
+    const uint64_t t0 = tile * kTile;
+    const uint64_t poff = s_poff[s];
+    const uint32_t shift = s_shift[s];
+    const bool full = tile < nfull;
+    const uint8_t* stage = smem + (size_t)s * kDecStage;
+    uint4 bv[kVec];
+    uint32_t bits[kVec], cnt[kVec], off[kVec];
+    if (full) {
+      mbar_wait(&full_bar[s], parity);
+#pragma unroll
+      for (int j = 0; j < kVec; ++j) {
+        bv[j] = reinterpret_cast<const uint4*>(stage)[j * kThreads + tid];
+        bits[j] = stage[kTileBytes + j * kThreads + tid];
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kVec; ++j) {
+        const uint64_t g = t0 / 8 + j * kThreads + tid;
+        const uint64_t e = g * 8;
+        uint4 b = make_uint4(0, 0, 0, 0);
+        uint32_t m = 0;
+        if (e < n) {
+          m = mask[g];
+          const uint32_t valid = (uint32_t)(n - e < 8 ? n - e : 8);
+          m &= (valid == 8) ? 0xffu : ((1u << valid) - 1u);
+          for (uint32_t k = 0; k < valid; ++k) set_u16_lane(b, k, base[e + k]);
+        }
+        bv[j] = b;
+        bits[j] = m;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kVec; ++j) cnt[j] = __popc(bits[j]);
+    tile_local_scan(cnt, off, s_warp, s_off);
+    const uint16_t* sp = reinterpret_cast<const uint16_t*>(stage + kTileBytes + kMaskBytes);
+#pragma unroll
+    for (int j = 0; j < kVec; ++j) {
+      uint32_t b = bits[j];
+      uint32_t r = off[j];
       uint4 v = bv[j];
       while (b) {
         const uint32_t k = __ffs(b) - 1;
         b &= b - 1;
-        if (pos < n_c) set_u16_lane(v, k, payload[pos]);
-        ++pos;
+        const uint64_t pos = poff + r;
+        uint32_t val;
+        if (shift != ~0u) val = sp[shift + r];
+        else val = pos < n_c ? payload[pos] : 0u;
+        set_u16_lane(v, k, val);
+        ++r;
       }
-      st_stream_v4(out + e, v);
-    } else {
-      for (uint32_t k = 0; k < 8; ++k) {
-        if (e + k >= n) break;
-        uint16_t v = base[e + k];
-        if ((b >> k) & 1u) {
-          if (pos < n_c) v = payload[pos];
-          ++pos;
-        }
-        out[e + k] = v;
+      const uint64_t e = t0 + (uint64_t)(j * kThreads + tid) * 8;
+      if (full) {
+        st_stream_v4(out + e, v);
+      } else {
+        for (uint32_t k = 0; k < 8 && e + k < n; ++k) out[e + k] = (uint16_t)u16_lane(v, k);
+      }
+    }
+    __syncthreads();  // every thread is done with stage s
+    if (tid == 0) refill(s, next_t, next_a, next_b);
+  }
+}
+
+// Apply with precomputed offsets, one CTA per tile (in-place chain replay and
+// the path for operands that are not 16-byte aligned).  In place it touches
+// only changed elements and never runs when validation raised a flag.
+template <bool kInPlace>
+__global__ void __launch_bounds__(kThreads)
+    delta_apply_kernel(const uint16_t* base, const uint8_t* __restrict__ mask,
+                       const uint16_t* __restrict__ payload, uint64_t n, uint64_t n_c,
+                       uint16_t* out, const uint64_t* __restrict__ offsets,
+                       const bsnp_status* __restrict__ st) {
+  __shared__ uint64_t s_warp[kWarps];
+  __shared__ uint32_t s_off[kVec][kWarps];
+  if (kInPlace && *(volatile const uint32_t*)&st->err_flags) return;
+  const uint64_t tile = blockIdx.x;
+  const uint64_t t0 = tile * kTile;
+  uint32_t bits[kVec], cnt[kVec], off[kVec];
+#pragma unroll
+  for (int j = 0; j < kVec; ++j) {
+    const uint64_t g = t0 / 8 + j * kThreads + threadIdx.x;
+    uint32_t m = 0;
+    if (g * 8 < n) {
+      m = __ldg(mask + g);
+      if (g * 8 + 8 > n) m &= (1u << (uint32_t)(n - g * 8)) - 1u;
+    }
+    bits[j] = m;
+    cnt[j] = __popc(m);
+  }
+  tile_local_scan(cnt, off, s_warp, s_off);
+  const uint64_t poff = offsets[tile];
+#pragma unroll
+  for (int j = 0; j < kVec; ++j) {
+    const uint32_t b = bits[j];
+    uint64_t pos = poff + off[j];
+    const uint64_t e = t0 + (uint64_t)(j * kThreads + threadIdx.x) * 8;
+    for (uint32_t k = 0; k < 8 && e + k < n; ++k) {
+      if ((b >> k) & 1u) {
+        if (pos < n_c) out[e + k] = payload[pos];
+        ++pos;
+      } else if (!kInPlace) {
+        out[e + k] = base[e + k];
       }
     }
   }
 }
 
+// persistent grid size for a dynamic-smem kernel
+template <typename K>
+int persistent_grid(K kernel, size_t smem, uint64_t work_items, int threads = kThreads) {
+  static int sms = -1;
+  if (sms < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+  if (per_sm < 1) per_sm = 1;
+  uint64_t g = (uint64_t)sms * per_sm;
+  if (g > work_items) g = work_items;
+  return (int)(g ? g : 1);
+}
+
+constexpr int kDecStages = 2;
 }  // namespace
 }  // namespace bsnp
 
 using namespace bsnp;
 
-extern "C" size_t bsnp_delta_ws_bytes(uint64_t n) {
-  return kWsHeader + 8 * (size_t)num_tiles(n);
+#ifdef BSNP_LOOKBACK_STATS
+extern "C" int bsnpdbg_lookback_stats(unsigned long long* out4, int reset) {
+  cudaMemcpyFromSymbol(out4, g_lookback_stats, sizeof(unsigned long long) * 4);
+  if (reset) {
+    unsigned long long z[4] = {0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_lookback_stats, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
+
+static size_t enc_scratch_offset(uint64_t n) {
+  return align_up(kWsHeader + 8 * (size_t)num_tiles(n), 256);
+}
+
+extern "C" size_t bsnp_delta_encode_ws_bytes(uint64_t n) {
+  // ticket | tile status words | payload staging slots (kTile per tile)
+  return enc_scratch_offset(n) + 2 * (size_t)num_tiles(n) * kTile;
+}
+
+extern "C" size_t bsnp_delta_decode_ws_bytes(uint64_t n) {
+  // ticket | chunk status words | tile payload offsets [ntiles + 1]
+  const uint64_t nt = num_tiles(n);
+  const uint64_t nchunks = (nt + kChunkTiles - 1) / kChunkTiles;
+  return kWsHeader + 8 * (size_t)nchunks + 8 * (size_t)(nt + 1);
 }
 
 extern "C" int bsnp_delta_encode(const uint16_t* base, const uint16_t* target, uint64_t n,
@@ -284,23 +718,28 @@ extern "C" int bsnp_delta_encode(const uint16_t* base, const uint16_t* target, u
   if (n && (!base || !target || !mask || !ws || (!payload && payload_cap)))
     return BSNP_E_INVALID;
   if (((uintptr_t)base | (uintptr_t)target | (uintptr_t)payload) & 1) return BSNP_E_ALIGN;
-  const size_t need = bsnp_delta_ws_bytes(n);
+  const size_t need = bsnp_delta_encode_ws_bytes(n);
   if (n && ws_bytes < need) return BSNP_E_WORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;
   int rc = cuda_status("memset(status)", cudaMemsetAsync(status, 0, sizeof(bsnp_status), s));
   if (rc || n == 0) return rc;
-  rc = cuda_status("memset(ws)", cudaMemsetAsync(ws, 0, need, s));
-  if (rc) return rc;
   const uint64_t nt = num_tiles(n);
+  rc = cuda_status("memset(ws)", cudaMemsetAsync(ws, 0, kWsHeader + 8 * nt, s));
+  if (rc) return rc;
   uint32_t* ticket = (uint32_t*)ws;
   uint64_t* tstat = (uint64_t*)((char*)ws + kWsHeader);
   const bool aligned = (((uintptr_t)base | (uintptr_t)target) & 15) == 0;
-  if (aligned)
-    delta_encode_kernel<true><<<(unsigned)nt, kThreads, 0, s>>>(
-        base, target, n, mask, payload, payload_cap, status, ticket, tstat, nt);
-  else
+  if (aligned) {
+    const size_t smem = (size_t)kEncStagesWS * kEncStage;
+    auto k = delta_encode_ws_kernel;
+    const int grid = persistent_grid(k, smem, nt, kEncThreads);
+    uint16_t* scratch = (uint16_t*)((char*)ws + enc_scratch_offset(n));
+    k<<<grid, kEncThreads, smem, s>>>(base, target, n, mask, payload, payload_cap, scratch,
+                                      status, ticket, tstat, nt);
+  } else {
     delta_encode_kernel<false><<<(unsigned)nt, kThreads, 0, s>>>(
         base, target, n, mask, payload, payload_cap, status, ticket, tstat, nt);
+  }
   return launch_status("delta_encode_kernel");
 }
 
@@ -312,35 +751,36 @@ extern "C" int bsnp_delta_decode(const uint16_t* base, const uint8_t* mask,
   if (n && (!base || !mask || !out || !ws || (!payload && n_c))) return BSNP_E_INVALID;
   if (n_c > n) return BSNP_E_INVALID;
   if (((uintptr_t)base | (uintptr_t)out | (uintptr_t)payload) & 1) return BSNP_E_ALIGN;
-  const size_t need = bsnp_delta_ws_bytes(n);
+  const size_t need = bsnp_delta_decode_ws_bytes(n);
   if (n && ws_bytes < need) return BSNP_E_WORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;
   int rc = cuda_status("memset(status)", cudaMemsetAsync(status, 0, sizeof(bsnp_status), s));
   if (rc || n == 0) return rc;
-  rc = cuda_status("memset(ws)", cudaMemsetAsync(ws, 0, need, s));
-  if (rc) return rc;
   const uint64_t nt = num_tiles(n);
+  const uint64_t nchunks = (nt + kChunkTiles - 1) / kChunkTiles;
   uint32_t* ticket = (uint32_t*)ws;
-  uint64_t* tstat = (uint64_t*)((char*)ws + kWsHeader);
+  uint32_t* ticket2 = (uint32_t*)ws + 32;
+  uint64_t* cstat = (uint64_t*)((char*)ws + kWsHeader);
+  uint64_t* offsets = cstat + nchunks;
+  rc = cuda_status("memset(ws)", cudaMemsetAsync(ws, 0, kWsHeader + 8 * nchunks, s));
+  if (rc) return rc;
+  // pass 1: payload offsets per tile + validation (reads n/8 bytes)
+  delta_offsets_kernel<<<(unsigned)nchunks, kThreads, 0, s>>>(mask, n, n_c, offsets, status,
+                                                              ticket, cstat, nchunks);
+  if ((rc = launch_status("delta_offsets_kernel"))) return rc;
   const bool in_place = (const void*)base == (const void*)out;
-  const bool aligned = (((uintptr_t)base | (uintptr_t)out) & 15) == 0;
+  const bool aligned = (((uintptr_t)base | (uintptr_t)out | (uintptr_t)mask) & 15) == 0;
   if (in_place) {
-    const uint64_t nbytes = (n + 7) / 8;
-    unsigned grid = (unsigned)((nbytes + 255) / 256);
-    const unsigned cap = 148u * 8u;
-    if (grid > cap) grid = cap;
-    delta_mask_check_kernel<<<grid, 256, 0, s>>>(mask, n, status);
-    if ((rc = launch_status("delta_mask_check_kernel"))) return rc;
-    delta_check_finish_kernel<<<1, 1, 0, s>>>(status, n_c);
-    if ((rc = launch_status("delta_check_finish_kernel"))) return rc;
-    delta_decode_kernel<false, true><<<(unsigned)nt, kThreads, 0, s>>>(
-        base, mask, payload, n, n_c, out, status, ticket, tstat, nt);
+    delta_apply_kernel<true><<<(unsigned)nt, kThreads, 0, s>>>(base, mask, payload, n, n_c,
+                                                                out, offsets, status);
   } else if (aligned) {
-    delta_decode_kernel<true, false><<<(unsigned)nt, kThreads, 0, s>>>(
-        base, mask, payload, n, n_c, out, status, ticket, tstat, nt);
+    const size_t smem = (size_t)kDecStages * kDecStage;
+    auto k = delta_decode_tma_kernel<kDecStages>;
+    const int grid = persistent_grid(k, smem, nt);
+    k<<<grid, kThreads, smem, s>>>(base, mask, payload, n, n_c, out, offsets, ticket2);
   } else {
-    delta_decode_kernel<false, false><<<(unsigned)nt, kThreads, 0, s>>>(
-        base, mask, payload, n, n_c, out, status, ticket, tstat, nt);
+    delta_apply_kernel<false><<<(unsigned)nt, kThreads, 0, s>>>(base, mask, payload, n, n_c,
+                                                                 out, offsets, status);
   }
   return launch_status("delta_decode_kernel");
 }

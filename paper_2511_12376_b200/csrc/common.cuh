@@ -49,6 +49,54 @@ __device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
 }
 
 // ---------------------------------------------------------------------------
+// TMA bulk copies (cp.async.bulk, SASS UBLKCP) completing on an mbarrier.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
+               : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+// global -> shared bulk copy; bytes multiple of 16, both addresses 16B aligned
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
+      : "memory");
+}
+
+// ---------------------------------------------------------------------------
 // Decoupled look-back over per-tile status words (single-pass prefix scan).
 // Word layout: [63:62] flag (0 = not ready, 1 = tile aggregate, 2 = inclusive
 // prefix), [61:0] value.  Flag and value live in one 64-bit word, so a
@@ -68,13 +116,24 @@ __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
   return v;
 }
 
+#ifdef BSNP_LOOKBACK_STATS
+__device__ unsigned long long g_lookback_stats[4];  // calls, windows, spins
+#endif
+
+// Publish a tile's aggregate (tile 0 publishes its inclusive prefix).
+__device__ __forceinline__ void publish_aggregate(uint64_t* status, uint64_t tile,
+                                                  uint64_t aggregate) {
+  st_relaxed_u64(status + tile, (tile == 0 ? kFlagInc : kFlagAgg) | aggregate);
+}
+
 __device__ __forceinline__ uint64_t lookback_exclusive(uint64_t* status, uint64_t tile,
-                                                       uint64_t aggregate, int lane) {
+                                                       uint64_t aggregate, int lane,
+                                                       bool publish_agg = true) {
   if (tile == 0) {
-    if (lane == 0) st_relaxed_u64(status, kFlagInc | aggregate);
+    if (lane == 0 && publish_agg) st_relaxed_u64(status, kFlagInc | aggregate);
     return 0;
   }
-  if (lane == 0) st_relaxed_u64(status + tile, kFlagAgg | aggregate);
+  if (lane == 0 && publish_agg) st_relaxed_u64(status + tile, kFlagAgg | aggregate);
   uint64_t excl = 0;
   int64_t top = (int64_t)tile - 1;
   while (true) {
@@ -89,14 +148,90 @@ __device__ __forceinline__ uint64_t lookback_exclusive(uint64_t* status, uint64_
       const int first = inc ? __ffs(inc) - 1 : 31;
       relevant = first == 31 ? kFull : ((2u << first) - 1u);
       if (!(bad & relevant)) break;
+#ifdef BSNP_LOOKBACK_STATS
+      if (lane == 0) atomicAdd(&g_lookback_stats[2], 1ull);
+#endif
       __nanosleep(32);
     }
+#ifdef BSNP_LOOKBACK_STATS
+    if (lane == 0) atomicAdd(&g_lookback_stats[1], 1ull);
+#endif
     const uint64_t v = (relevant >> lane) & 1u ? (s & kValMask) : 0;
     excl += warp_sum_u64(v);
     if (inc) break;
     top -= 32;
   }
   if (lane == 0) st_relaxed_u64(status + tile, kFlagInc | (excl + aggregate));
+#ifdef BSNP_LOOKBACK_STATS
+  if (lane == 0) atomicAdd(&g_lookback_stats[0], 1ull);
+#endif
+  return excl;
+}
+
+// Wide look-back: each round trip inspects kW*32 predecessors (element
+// distance d = k*32 + lane + 1 for k = 0..kW-1).  The tile's own aggregate must
+// already be published (publish_aggregate).  Returns the exclusive prefix on
+// every lane and publishes the inclusive prefix.
+#ifndef BSNP_SPIN_NS
+#define BSNP_SPIN_NS 512
+#endif
+template <int kW>
+__device__ __forceinline__ uint64_t lookback_wide(uint64_t* status, uint64_t tile,
+                                                  uint64_t aggregate, int lane) {
+  if (tile == 0) return 0;
+  uint64_t excl = 0;
+  int64_t top = (int64_t)tile - 1;
+  uint32_t backoff = BSNP_SPIN_NS;
+  while (true) {
+    uint64_t sv[kW];
+    uint32_t incm[kW], badm[kW];
+    int kf, lf;
+    while (true) {
+#pragma unroll
+      for (int k = 0; k < kW; ++k) {
+        const int64_t idx = top - (k * 32 + lane);
+        sv[k] = idx >= 0 ? ld_relaxed_u64(status + idx) : kFlagInc;
+      }
+      kf = kW;
+      lf = 31;
+#pragma unroll
+      for (int k = kW - 1; k >= 0; --k) {
+        const uint32_t fl = (uint32_t)(sv[k] >> 62);
+        incm[k] = __ballot_sync(kFull, fl == 2);
+        badm[k] = __ballot_sync(kFull, fl == 0);
+        if (incm[k]) {
+          kf = k;
+          lf = __ffs(incm[k]) - 1;
+        }
+      }
+      bool bad = false;
+#pragma unroll
+      for (int k = 0; k < kW; ++k) {
+        const uint32_t rel = k < kf ? kFull : (k == kf ? (lf == 31 ? kFull : ((2u << lf) - 1u)) : 0u);
+        bad |= (badm[k] & rel) != 0;
+      }
+#ifdef BSNP_LOOKBACK_STATS
+      if (bad && lane == 0) atomicAdd(&g_lookback_stats[2], 1ull);
+#endif
+      if (!bad) break;
+      __nanosleep(backoff);  // exponential back-off keeps spinners off the hot L2 lines
+      if (backoff < 4096) backoff *= 2;
+    }
+#ifdef BSNP_LOOKBACK_STATS
+    if (lane == 0) atomicAdd(&g_lookback_stats[1], 1ull);
+#endif
+    uint64_t v = 0;
+#pragma unroll
+    for (int k = 0; k < kW; ++k)
+      if (k < kf || (k == kf && lane <= lf)) v += sv[k] & kValMask;
+    excl += warp_sum_u64(v);
+    if (kf < kW) break;
+    top -= 32 * kW;
+  }
+  if (lane == 0) st_relaxed_u64(status + tile, kFlagInc | (excl + aggregate));
+#ifdef BSNP_LOOKBACK_STATS
+  if (lane == 0) atomicAdd(&g_lookback_stats[0], 1ull);
+#endif
   return excl;
 }
 

@@ -196,7 +196,7 @@ def test_payload_cap_flag(dev):
     mask = torch.empty((n + 7) // 8, dtype=torch.uint8, device=dev)
     payload = torch.full((100,), -1, dtype=torch.int16, device=dev)
     st = rt.new_status(dev)
-    ws = torch.empty(_lib.load().bsnp_delta_ws_bytes(n), dtype=torch.uint8, device=dev)
+    ws = torch.empty(_lib.load().bsnp_delta_encode_ws_bytes(n), dtype=torch.uint8, device=dev)
     rc = _lib.load().bsnp_delta_encode(b.data_ptr(), c.data_ptr(), n, mask.data_ptr(),
                                        payload.data_ptr(), 100, st.data_ptr(),
                                        ws.data_ptr(), ws.numel(),

@@ -37,9 +37,11 @@ def test_library_exports_every_declared_symbol():
 def test_ws_sizes_without_gpu():
     from paper_2511_12376_b200 import _lib
     lib = _lib.load()
-    assert lib.bsnp_delta_ws_bytes(0) == 256
-    assert lib.bsnp_delta_ws_bytes(8192) == 256 + 8
-    assert lib.bsnp_delta_ws_bytes(8193) == 256 + 16
+    for n in (0, 1, 8192, 8193, 1 << 30):
+        nt = -(-n // 8192)
+        # header + tile status (256-aligned) + 16 KiB payload staging per tile
+        assert lib.bsnp_delta_encode_ws_bytes(n) == -(-(256 + 8 * nt) // 256) * 256 + 16384 * nt
+        assert lib.bsnp_delta_decode_ws_bytes(n) == 256 + 8 * -(-nt // 32) + 8 * (nt + 1)
 
 
 def test_argument_errors_without_gpu():
