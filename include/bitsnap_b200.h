@@ -92,6 +92,74 @@ int bsnp_delta_decode(const uint16_t* base, const uint8_t* mask, const uint16_t*
                       uint64_t n, uint64_t n_c, uint16_t* out, bsnp_status* status,
                       void* ws, size_t ws_bytes, void* stream);
 
+/* ------------------------------------------------------------------------
+ * Cluster quantizer (reference quantizer.py:100-204)
+ *
+ * A "unit" is the slice that gets its own ClusterTable: the whole tensor when
+ * block == 0 (the reference's per-tensor behaviour, store.py:261-263) or
+ * consecutive `block`-element slices (block % 8 == 0; the last slice may be
+ * shorter), the per-block mode of BASELINE configs[2] whose oracle is the
+ * reference applied to each slice.  Units are laid out back to back:
+ *   tables[u]                  one bsnp_cluster_table per unit
+ *   labels  + u * block / 2    packed 4-bit labels of unit u (ceil(len/2) B,
+ *                              low nibble = even index, quantizer.py:146-150)
+ *   codes   + u * block        one u8 code per element
+ * ---------------------------------------------------------------------- */
+
+/* ClusterTable (quantizer.py:45-65) in device memory, 256 bytes. */
+typedef struct bsnp_cluster_table {
+  float mean;            /* f32(mean), quantizer.py:350, 368 */
+  float std;             /* f32(std),  quantizer.py:351, 369 */
+  float boundaries[15];  /* m-1 used: f32(mu + std * ndtri(k/m)) */
+  float scales[16];      /* m used: f32(max - min) per cluster, 0 if empty */
+  float offsets[16];     /* m used: f32(min) per cluster, 0 if empty */
+  uint32_t m;            /* clusters, 2..16 */
+  uint32_t flags;        /* BSNP_ERR_NONFINITE if the unit had NaN/Inf statistics */
+  uint32_t reserved[13];
+} bsnp_cluster_table;
+
+/* Workspace of a fit / quantize / dequantize call over n elements. */
+size_t bsnp_cluster_ws_bytes(uint64_t n, uint64_t block);
+
+/*
+ * Replaces build_clusters (quantizer.py:100-135) for every unit: mean/std in
+ * float64 with numpy's pairwise summation tree reproduced exactly, normal-
+ * quantile boundaries, per-cluster min/max with fit-time labels taken against
+ * the unrounded float64 boundaries.  Bit-identical tables.
+ */
+int bsnp_cluster_fit(const float* x, uint64_t n, uint64_t block, int m,
+                     bsnp_cluster_table* tables, void* ws, size_t ws_bytes, void* stream);
+
+/*
+ * Replaces quantize (quantizer.py:161-189) for every unit with the given
+ * tables: label = #(boundaries < v), code = ceil(clip((v-b)/S,0,1)*255 - 0.5)
+ * evaluated exactly as the reference's float64 expression.
+ */
+int bsnp_cluster_quantize(const float* x, uint64_t n, uint64_t block,
+                          const bsnp_cluster_table* tables, uint8_t* labels, uint8_t* codes,
+                          void* ws, size_t ws_bytes, void* stream);
+
+/* fit + quantize in one call (the store's optimizer-state path). */
+int bsnp_cluster_encode(const float* x, uint64_t n, uint64_t block, int m,
+                        bsnp_cluster_table* tables, uint8_t* labels, uint8_t* codes,
+                        void* ws, size_t ws_bytes, void* stream);
+
+/*
+ * Replaces dequantize (quantizer.py:192-204): out = f32(f64(code)/255 * S + b).
+ * status->count = largest label seen; BSNP_ERR_LABEL if it is >= m.
+ */
+int bsnp_cluster_dequantize(const uint8_t* labels, const uint8_t* codes, uint64_t n,
+                            uint64_t block, const bsnp_cluster_table* tables, float* out,
+                            bsnp_status* status, void* ws, size_t ws_bytes, void* stream);
+
+/*
+ * Reduction behind precision_report (quantizer.py:280-296): acc3 receives
+ * { sum (o-r)^2, sum |o-r|/|o| over |o| > 1e-12, count of |o| > 1e-12 } in
+ * float64 (MSE = acc3[0]/n, MRE = acc3[1]/acc3[2]).
+ */
+int bsnp_precision_report(const float* original, const float* restored, uint64_t n,
+                          double* acc3, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -28,6 +28,12 @@ SIGNATURES = {
     "bsnp_delta_decode_ws_bytes": (_sz, [_u64]),
     "bsnp_delta_encode": (_i32, [_vp, _vp, _u64, _vp, _vp, _u64, _vp, _vp, _sz, _vp]),
     "bsnp_delta_decode": (_i32, [_vp, _vp, _vp, _u64, _u64, _vp, _vp, _vp, _sz, _vp]),
+    "bsnp_cluster_ws_bytes": (_sz, [_u64, _u64]),
+    "bsnp_cluster_fit": (_i32, [_vp, _u64, _u64, _i32, _vp, _vp, _sz, _vp]),
+    "bsnp_cluster_quantize": (_i32, [_vp, _u64, _u64, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "bsnp_cluster_encode": (_i32, [_vp, _u64, _u64, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "bsnp_cluster_dequantize": (_i32, [_vp, _vp, _u64, _u64, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "bsnp_precision_report": (_i32, [_vp, _vp, _u64, _vp, _vp]),
 }
 
 _lock = threading.Lock()

@@ -1,0 +1,730 @@
+// Cluster quantizer for sm_100a.
+//
+// Replaces build_clusters / quantize / dequantize of the reference
+// (/root/reference/pkg/src/bitsnap/quantizer.py:100-204) with bit-identical
+// results:
+//
+//  * fit statistics: numpy computes mean and std of the float64-widened
+//    tensor with pairwise summation (np.add.reduce over a contiguous vector,
+//    numpy/_core/src/umath/loops_utils.h.src): a node of s > 128 elements
+//    splits at 8*floor(s/16); a leaf of <= 128 elements is summed with 8
+//    interleaved accumulators combined as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7))
+//    plus a sequential tail; a node of < 8 elements sums sequentially from 0.
+//    The kernels reproduce that tree exactly: a unit is cut into the 2^D
+//    nodes of depth D (<= kTileMax elements each, one CTA per node), every
+//    CTA evaluates its node's sub-tree in shared memory (a heap of <= 255
+//    nodes: leaves by 4-lane groups, then level-wise combines), and one CTA
+//    per unit combines the 2^D partials as a perfect binary tree.
+//  * fit labels use the unrounded float64 boundaries; for a float32 value v,
+//    B64 < v  <=>  RD_f32(B64) < v, so the comparison runs in float32.
+//  * quantize codes: a float32 estimate of ceil(255 (v-b)/S - 0.5) is exact
+//    whenever its argument is farther than 2^-12 from an integer (the
+//    estimate's error is < 6.2e-5); the rare ambiguous
+//    elements evaluate the reference's float64 expression.
+//  * dequantize: a per-unit 16 x 256 LUT of f32(f64(j)/255 * S + b).
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "ndtri_table.cuh"
+#include "runtime.cuh"
+
+namespace bsnp {
+namespace {
+
+constexpr int kQThreads = 256;
+constexpr uint32_t kTileMax = 8192;  // elements per tree tile (a depth-D node)
+constexpr int kHeapDepth = 7;        // leaves of a <= kTileMax node lie at depth <= 7
+constexpr int kHeap = 1 << (kHeapDepth + 1);
+constexpr uint32_t kSmemFloats = kTileMax + (kTileMax / 128) * 8 + 32;
+constexpr uint32_t kDqChunk = 65536;  // elements per dequantize CTA (one LUT build)
+static_assert(sizeof(bsnp_cluster_table) == 256, "table layout is part of the C-ABI");
+
+// shared-memory layout: 8 floats of padding per 128-float chunk so that the
+// 4-lane leaf groups of a warp hit distinct banks
+__device__ __forceinline__ uint32_t padded(uint32_t i) { return i + ((i >> 7) << 3); }
+
+struct QPlan {
+  uint64_t n, block;  // block = unit length (n for one unit)
+  uint64_t last_len;
+  uint64_t total_tiles;
+  uint32_t nunits, m;
+  uint32_t D_full, T_full;  // tree depth / tiles of a full unit
+  uint32_t D_last, T_last;  // of the last unit
+  uint32_t C_full, C_last;  // dequantize chunks per unit
+};
+
+struct TileRef {
+  uint32_t u, j, D;
+  uint64_t len, ustart, off, size;
+};
+
+__device__ __forceinline__ TileRef locate(const QPlan& P, uint64_t tile) {
+  TileRef r;
+  const uint64_t full_tiles = (uint64_t)(P.nunits - 1) * P.T_full;
+  if (tile < full_tiles) {
+    r.u = (uint32_t)(tile / P.T_full);
+    r.j = (uint32_t)(tile % P.T_full);
+    r.D = P.D_full;
+    r.len = P.block;
+  } else {
+    r.u = P.nunits - 1;
+    r.j = (uint32_t)(tile - full_tiles);
+    r.D = P.D_last;
+    r.len = P.last_len;
+  }
+  r.ustart = (uint64_t)r.u * P.block;
+  uint64_t off = 0, size = r.len;
+  for (int b = (int)r.D - 1; b >= 0; --b) {
+    const uint64_t L = 8 * (size / 16);
+    if ((r.j >> b) & 1u) {
+      off += L;
+      size -= L;
+    } else {
+      size = L;
+    }
+  }
+  r.off = off;
+  r.size = size;
+  return r;
+}
+
+// order-preserving float -> int key (for min / max through integer atomics)
+__device__ __forceinline__ int fkey(float f) {
+  const int b = __float_as_int(f);
+  return b >= 0 ? b : b ^ 0x7fffffff;
+}
+__device__ __forceinline__ float fkey_inv(int k) {
+  return __int_as_float(k >= 0 ? k : k ^ 0x7fffffff);
+}
+
+// #(t[k] < v) over a sorted 16-slot table (unused slots hold +inf)
+__device__ __forceinline__ uint32_t count_below(const float* t, float v) {
+  uint32_t lo = 0;
+  lo += (t[lo + 7] < v) ? 8u : 0u;
+  lo += (t[lo + 3] < v) ? 4u : 0u;
+  lo += (t[lo + 1] < v) ? 2u : 0u;
+  lo += (t[lo] < v) ? 1u : 0u;
+  return lo;
+}
+
+// Load elements [0, size) of a tile into padded shared memory.
+__device__ __forceinline__ void load_tile(float* s, const float* src, uint32_t size) {
+  if (((uintptr_t)src & 15) == 0) {
+    const uint32_t nv = size / 4;
+    for (uint32_t v = threadIdx.x; v < nv; v += blockDim.x) {
+      const float4 x = ld_stream_f4(src + 4 * v);
+      *reinterpret_cast<float4*>(&s[padded(4 * v)]) = x;
+    }
+    for (uint32_t i = nv * 4 + threadIdx.x; i < size; i += blockDim.x) s[padded(i)] = src[i];
+  } else {
+    for (uint32_t i = threadIdx.x; i < size; i += blockDim.x) s[padded(i)] = src[i];
+  }
+}
+
+template <bool kVar>
+__device__ __forceinline__ double widen(float x, double mu) {
+  const double d = (double)x;
+  if (!kVar) return d;
+  const double c = __dsub_rn(d, mu);  // arr - arrmean
+  return __dmul_rn(c, c);             // x * x
+}
+
+struct Heap {
+  uint16_t off[kHeap];
+  uint16_t size[kHeap];
+  uint8_t kind[kHeap];  // 0 absent, 1 leaf, 2 internal
+  double val[kHeap];
+};
+
+// numpy pairwise sum of values widen(s[0..size)) — the sub-tree of one node.
+template <bool kVar>
+__device__ double tree_sum(const float* s, uint32_t size, double mu, Heap& H) {
+  const int tid = threadIdx.x;
+  for (int h = tid; h < kHeap; h += blockDim.x) {
+    if (h == 0) continue;
+    const int d = 31 - __clz(h);
+    const uint32_t j = (uint32_t)h - (1u << d);
+    uint32_t off = 0, sz = size;
+    bool present = true;
+    for (int b = d - 1; b >= 0; --b) {
+      if (sz <= 128) {
+        present = false;
+        break;
+      }
+      const uint32_t L = 8 * (sz / 16);
+      if ((j >> b) & 1u) {
+        off += L;
+        sz -= L;
+      } else {
+        sz = L;
+      }
+    }
+    H.kind[h] = !present ? 0 : (sz <= 128 ? 1 : 2);
+    H.off[h] = (uint16_t)off;
+    H.size[h] = (uint16_t)sz;
+  }
+  __syncthreads();
+  // leaves: 4 lanes per leaf, lane q owns accumulators r[2q], r[2q+1]
+  const int g = tid >> 2, q = tid & 3;
+  const int ngroups = blockDim.x >> 2;
+  const unsigned gm = 0xfu << ((tid & 31) & ~3);
+  for (int base = 0; base < kHeap; base += ngroups) {
+    const int h = base + g;
+    if (h == 0 || h >= kHeap || H.kind[h] != 1) continue;
+    const uint32_t off = H.off[h], sz = H.size[h];
+    double res = 0.0;
+    if (sz < 8) {
+      if (q == 0)
+        for (uint32_t i = 0; i < sz; ++i) res = __dadd_rn(res, widen<kVar>(s[padded(off + i)], mu));
+    } else {
+      const uint32_t body = sz - sz % 8;
+      float2 p = *reinterpret_cast<const float2*>(&s[padded(off + 2 * q)]);
+      double ra = widen<kVar>(p.x, mu), rb = widen<kVar>(p.y, mu);
+      for (uint32_t i = 8; i < body; i += 8) {
+        p = *reinterpret_cast<const float2*>(&s[padded(off + i + 2 * q)]);
+        ra = __dadd_rn(ra, widen<kVar>(p.x, mu));
+        rb = __dadd_rn(rb, widen<kVar>(p.y, mu));
+      }
+      double pr = __dadd_rn(ra, rb);
+      pr = __dadd_rn(pr, __shfl_xor_sync(gm, pr, 1));
+      pr = __dadd_rn(pr, __shfl_xor_sync(gm, pr, 2));
+      res = pr;
+      if (q == 0)
+        for (uint32_t i = body; i < sz; ++i) res = __dadd_rn(res, widen<kVar>(s[padded(off + i)], mu));
+    }
+    if (q == 0) H.val[h] = res;
+  }
+  for (int d = kHeapDepth - 1; d >= 0; --d) {
+    __syncthreads();
+    for (int h = (1 << d) + tid; h < (2 << d); h += blockDim.x)
+      if (H.kind[h] == 2) H.val[h] = __dadd_rn(H.val[2 * h], H.val[2 * h + 1]);
+  }
+  __syncthreads();
+  return H.val[1];
+}
+
+// pass 1 / pass 2 of the fit: per-tile pairwise sums of x (kVar = false) or
+// of (x - mean)^2 (kVar = true)
+template <bool kVar>
+__global__ void __launch_bounds__(kQThreads)
+    fit_tree_kernel(const float* __restrict__ x, QPlan P, const double* __restrict__ mu,
+                    double* __restrict__ partials) {
+  __shared__ __align__(16) float s[kSmemFloats];
+  __shared__ Heap H;
+  const TileRef r = locate(P, blockIdx.x);
+  load_tile(s, x + r.ustart + r.off, (uint32_t)r.size);
+  __syncthreads();
+  const double m = kVar ? mu[r.u] : 0.0;
+  const double v = tree_sum<kVar>(s, (uint32_t)r.size, m, H);
+  if (threadIdx.x == 0) partials[blockIdx.x] = v;
+}
+
+// Sum of the 2^D partials of one unit as a perfect binary tree.
+__device__ double combine_perfect(const double* p, uint32_t T, double* sv) {
+  const int tid = threadIdx.x;
+  const uint32_t lanes = T < (uint32_t)blockDim.x ? T : blockDim.x;
+  if ((uint32_t)tid < lanes) {
+    const uint32_t chunk = T / lanes;  // power of two
+    const double* c = p + (uint64_t)tid * chunk;
+    // left-to-right binary-counter reduction == perfect tree over the chunk
+    double stk[20];
+    uint32_t lvl[20];
+    int top = 0;
+    for (uint32_t i = 0; i < chunk; ++i) {
+      double v = c[i];
+      uint32_t l = 0;
+      while (top > 0 && lvl[top - 1] == l) {
+        v = __dadd_rn(stk[top - 1], v);
+        --top;
+        ++l;
+      }
+      stk[top] = v;
+      lvl[top] = l;
+      ++top;
+    }
+    sv[tid] = stk[0];
+  }
+  __syncthreads();
+  for (uint32_t w = lanes / 2; w >= 1; w /= 2) {
+    double a = 0.0;
+    if ((uint32_t)tid < w) a = __dadd_rn(sv[2 * tid], sv[2 * tid + 1]);
+    __syncthreads();
+    if ((uint32_t)tid < w) sv[tid] = a;
+    __syncthreads();
+  }
+  return sv[0];
+}
+
+__device__ __forceinline__ void unit_shape(const QPlan& P, uint32_t u, uint32_t& T,
+                                           uint64_t& len) {
+  const bool last = u == P.nunits - 1;
+  T = last ? P.T_last : P.T_full;
+  len = last ? P.last_len : P.block;
+}
+
+template <bool kVar>
+__global__ void __launch_bounds__(kQThreads)
+    fit_combine_kernel(QPlan P, const double* __restrict__ partials, double* __restrict__ mu,
+                       float* __restrict__ fthr, bsnp_cluster_table* __restrict__ tables) {
+  __shared__ double sv[kQThreads];
+  const uint32_t u = blockIdx.x;
+  uint32_t T;
+  uint64_t len;
+  unit_shape(P, u, T, len);
+  const double S = combine_perfect(partials + (uint64_t)u * P.T_full, T, sv);
+  if (threadIdx.x != 0) return;
+  const double mean = __ddiv_rn(__dadd_rn(0.0, S), (double)len);  // np.mean
+  bsnp_cluster_table& tb = tables[u];
+  if (!kVar) {
+    mu[u] = mean;
+    return;
+  }
+  const double m0 = mu[u];
+  const double var = __ddiv_rn(__dadd_rn(0.0, S), (double)len);
+  const double sd = __dsqrt_rn(var);  // np.std, ddof = 0
+  const int m = (int)P.m;
+  tb.mean = __double2float_rn(m0);
+  tb.std = __double2float_rn(sd);
+  tb.m = (uint32_t)m;
+  tb.flags = (isfinite(m0) && isfinite(sd)) ? 0u : BSNP_ERR_NONFINITE;
+  for (int k = 0; k < 15; ++k) {
+    if (k < m - 1) {
+      const double b = __dadd_rn(m0, __dmul_rn(sd, kNdtri[m][k]));  // mu + sigma * ndtri
+      tb.boundaries[k] = __double2float_rn(b);
+      fthr[u * 16 + k] = __double2float_rd(b);  // fit labels compare against b exactly
+    } else {
+      tb.boundaries[k] = 0.0f;
+      fthr[u * 16 + k] = __int_as_float(0x7f800000);
+    }
+  }
+  fthr[u * 16 + 15] = __int_as_float(0x7f800000);
+  for (int k = 0; k < 13; ++k) tb.reserved[k] = 0;
+}
+
+// pass 3 of the fit: per-tile, per-cluster min / max with fit-time labels
+__global__ void __launch_bounds__(kQThreads)
+    fit_minmax_kernel(const float* __restrict__ x, QPlan P, const float* __restrict__ fthr,
+                      int* __restrict__ tile_mm) {
+  __shared__ float thr[16];
+  __shared__ int smin[16], smax[16];
+  const TileRef r = locate(P, blockIdx.x);
+  const int tid = threadIdx.x;
+  if (tid < 16) {
+    thr[tid] = fthr[r.u * 16 + tid];
+    smin[tid] = 0x7fffffff;
+    smax[tid] = (int)0x80000000;
+  }
+  __syncthreads();
+  const float* src = x + r.ustart + r.off;
+  const uint32_t size = (uint32_t)r.size;
+  auto visit = [&](float v) {
+    const uint32_t c = count_below(thr, v);
+    const int k = fkey(v);
+    if (k < smin[c]) atomicMin(&smin[c], k);
+    if (k > smax[c]) atomicMax(&smax[c], k);
+  };
+  if (((uintptr_t)src & 15) == 0) {
+    const uint32_t nv = size / 4;
+    for (uint32_t i = tid; i < nv; i += blockDim.x) {
+      const float4 v = ld_stream_f4(src + 4 * i);
+      visit(v.x);
+      visit(v.y);
+      visit(v.z);
+      visit(v.w);
+    }
+    for (uint32_t i = nv * 4 + tid; i < size; i += blockDim.x) visit(src[i]);
+  } else {
+    for (uint32_t i = tid; i < size; i += blockDim.x) visit(src[i]);
+  }
+  __syncthreads();
+  if (tid < 16) {
+    tile_mm[blockIdx.x * 32 + tid] = smin[tid];
+    tile_mm[blockIdx.x * 32 + 16 + tid] = smax[tid];
+  }
+}
+
+// scales / offsets per unit (quantizer.py:117-125)
+__global__ void __launch_bounds__(kQThreads)
+    fit_finalize_kernel(QPlan P, const int* __restrict__ tile_mm,
+                        bsnp_cluster_table* __restrict__ tables) {
+  __shared__ int rmin[8][16], rmax[8][16];
+  const uint32_t u = blockIdx.x;
+  uint32_t T;
+  uint64_t len;
+  unit_shape(P, u, T, len);
+  const int c = threadIdx.x & 15, row = threadIdx.x >> 4;  // 16 rows x 16 clusters
+  int mn = 0x7fffffff, mx = (int)0x80000000;
+  const int* base = tile_mm + (uint64_t)u * P.T_full * 32;
+  for (uint32_t t = row; t < T; t += 16) {
+    mn = min(mn, base[t * 32 + c]);
+    mx = max(mx, base[t * 32 + 16 + c]);
+  }
+  // fold 16 rows -> 8 via shuffles inside the warp (rows r and r+1 share a warp)
+  mn = min(mn, __shfl_down_sync(kFull, mn, 16));
+  mx = max(mx, __shfl_down_sync(kFull, mx, 16));
+  if ((threadIdx.x & 31) < 16) {
+    rmin[threadIdx.x >> 5][c] = mn;
+    rmax[threadIdx.x >> 5][c] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x < 16) {
+    int a = rmin[0][c], b = rmax[0][c];
+    for (int w = 1; w < 8; ++w) {
+      a = min(a, rmin[w][c]);
+      b = max(b, rmax[w][c]);
+    }
+    bsnp_cluster_table& tb = tables[u];
+    float scale = 0.0f, offset = 0.0f;
+    if ((uint32_t)c < P.m && a <= b) {
+      const float lo = fkey_inv(a), hi = fkey_inv(b);
+      scale = __double2float_rn(__dsub_rn((double)hi, (double)lo));
+      offset = lo;
+    }
+    tb.scales[c] = scale;
+    tb.offsets[c] = offset;
+  }
+}
+
+// ----------------------------------------------------------------- quantize
+struct QuantParams {
+  float bnd[16];  // boundaries, +inf padded
+  float off[16];  // cluster min
+  float rcp[16];  // 255 / S (0 if S == 0, NaN if not finite -> exact path)
+  float scl[16];  // S
+  uint32_t last;  // m - 1: numpy's searchsorted sorts NaN after every boundary
+};
+
+__device__ __forceinline__ void load_quant_params(const bsnp_cluster_table& tb, QuantParams& Q) {
+  const int t = threadIdx.x;
+  if (t < 16) {
+    const uint32_t m = tb.m;
+    Q.bnd[t] = ((uint32_t)t < m - 1) ? tb.boundaries[t] : __int_as_float(0x7f800000);
+    const float S = tb.scales[t];
+    Q.scl[t] = S;
+    Q.off[t] = tb.offsets[t];
+    float rc = 0.0f;
+    if (S > 0.0f) {
+      rc = __fdiv_rn(255.0f, S);
+      if (!isfinite(rc)) rc = __int_as_float(0x7fffffff);
+    }
+    Q.rcp[t] = rc;
+    if (t == 0) Q.last = m - 1;
+  }
+}
+
+// exact code of quantizer.py:174-182 in float64 (the slow path)
+__device__ __noinline__ uint32_t exact_code(float v, float b, float S) {
+  double xn = 0.0;
+  if (S > 0.0f) xn = __ddiv_rn(__dsub_rn((double)v, (double)b), (double)S);
+  xn = fmin(fmax(xn, 0.0), 1.0);
+  const double y = __dsub_rn(__dmul_rn(xn, 255.0), 0.5);
+  double c = ceil(y);
+  c = fmin(fmax(c, 0.0), 255.0);
+  return (uint32_t)c;
+}
+
+__device__ __forceinline__ uint32_t quant_one(const QuantParams& Q, float v, uint32_t& label) {
+  const uint32_t c = isnan(v) ? Q.last : count_below(Q.bnd, v);
+  label = c;
+  const float b = Q.off[c];
+  const float t = __fsub_rn(__fmul_rn(__fsub_rn(v, b), Q.rcp[c]), 0.5f);
+  // the float32 estimate t is within 6.2e-5 of 255(v-b)/S - 0.5
+  const bool amb = isnan(t) || fabsf(__fsub_rn(t, rintf(t))) <= 0.000244140625f;
+  if (__builtin_expect(amb, 0)) return exact_code(v, b, Q.scl[c]);
+  int e = __float2int_ru(t);
+  e = e < 0 ? 0 : (e > 255 ? 255 : e);
+  return (uint32_t)e;
+}
+
+__global__ void __launch_bounds__(kQThreads)
+    quantize_kernel(const float* __restrict__ x, QPlan P,
+                    const bsnp_cluster_table* __restrict__ tables, uint8_t* __restrict__ labels,
+                    uint8_t* __restrict__ codes) {
+  __shared__ QuantParams Q;
+  const TileRef r = locate(P, blockIdx.x);
+  load_quant_params(tables[r.u], Q);
+  __syncthreads();
+  const float* src = x + r.ustart + r.off;
+  uint8_t* cdst = codes + r.ustart + r.off;
+  uint8_t* ldst = labels + (uint64_t)r.u * (P.block / 2) + r.off / 2;
+  const uint32_t size = (uint32_t)r.size;
+  const bool vec = (((uintptr_t)src & 15) | ((uintptr_t)cdst & 3) | ((uintptr_t)ldst & 1)) == 0;
+  const uint32_t nv = vec ? size / 4 : 0;
+  for (uint32_t i = threadIdx.x; i < nv; i += blockDim.x) {
+    const float4 v = ld_stream_f4(src + 4 * i);
+    uint32_t l0, l1, l2, l3;
+    const uint32_t c0 = quant_one(Q, v.x, l0), c1 = quant_one(Q, v.y, l1);
+    const uint32_t c2 = quant_one(Q, v.z, l2), c3 = quant_one(Q, v.w, l3);
+    *reinterpret_cast<uint32_t*>(cdst + 4 * i) = c0 | (c1 << 8) | (c2 << 16) | (c3 << 24);
+    *reinterpret_cast<uint16_t*>(ldst + 2 * i) =
+        (uint16_t)((l0 | (l1 << 4)) | ((l2 | (l3 << 4)) << 8));
+  }
+  // tail (and unaligned tiles): element pairs
+  for (uint32_t p = nv * 2 + threadIdx.x; 2 * p < size; p += blockDim.x) {
+    uint32_t la, lb = 0;
+    cdst[2 * p] = (uint8_t)quant_one(Q, src[2 * p], la);
+    if (2 * p + 1 < size) cdst[2 * p + 1] = (uint8_t)quant_one(Q, src[2 * p + 1], lb);
+    ldst[p] = (uint8_t)(la | (lb << 4));
+  }
+}
+
+// --------------------------------------------------------------- dequantize
+__global__ void __launch_bounds__(kQThreads)
+    dequantize_kernel(const uint8_t* __restrict__ labels, const uint8_t* __restrict__ codes,
+                      QPlan P, const bsnp_cluster_table* __restrict__ tables,
+                      float* __restrict__ out, bsnp_status* __restrict__ st) {
+  __shared__ float lut[16 * 256];
+  __shared__ uint32_t s_maxlab;
+  // chunk -> (unit, element range)
+  const uint64_t cidx = blockIdx.x;
+  const uint64_t full_chunks = (uint64_t)(P.nunits - 1) * P.C_full;
+  uint32_t u;
+  uint64_t c0, len;
+  if (cidx < full_chunks) {
+    u = (uint32_t)(cidx / P.C_full);
+    c0 = (cidx % P.C_full) * kDqChunk;
+    len = P.block;
+  } else {
+    u = P.nunits - 1;
+    c0 = (cidx - full_chunks) * kDqChunk;
+    len = P.last_len;
+  }
+  const uint64_t c1 = c0 + kDqChunk < len ? c0 + kDqChunk : len;
+  const bsnp_cluster_table& tb = tables[u];
+  const uint32_t m = tb.m;
+  if (threadIdx.x == 0) s_maxlab = 0;
+  for (uint32_t i = threadIdx.x; i < 16 * 256; i += blockDim.x) {
+    const uint32_t c = i >> 8, j = i & 255;
+    // restored = (qmap(code) * S + b).astype(float32)   (quantizer.py:199-201)
+    lut[i] = c < m ? __double2float_rn(__dadd_rn(__dmul_rn(kQmap[j], (double)tb.scales[c]),
+                                                 (double)tb.offsets[c]))
+                   : 0.0f;
+  }
+  __syncthreads();
+  const uint64_t ustart = (uint64_t)u * P.block;
+  const uint8_t* cs = codes + ustart;
+  const uint8_t* ls = labels + (uint64_t)u * (P.block / 2);
+  float* o = out + ustart;
+  uint32_t maxlab = 0;
+  const bool vec = ((((uintptr_t)(cs + c0)) & 7) | (((uintptr_t)(ls + c0 / 2)) & 3) |
+                    (((uintptr_t)(o + c0)) & 15)) == 0;
+  uint64_t e = c0;
+  if (vec) {
+    const uint64_t nv = (c1 - c0) / 8;
+    for (uint64_t i = threadIdx.x; i < nv; i += blockDim.x) {
+      const uint64_t e0 = c0 + 8 * i;
+      const uint2 cc = *reinterpret_cast<const uint2*>(cs + e0);
+      const uint32_t ll = *reinterpret_cast<const uint32_t*>(ls + e0 / 2);
+      float r[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t lab = (ll >> (4 * k)) & 15u;
+        const uint32_t code = ((k < 4 ? cc.x : cc.y) >> (8 * (k & 3))) & 255u;
+        maxlab = lab > maxlab ? lab : maxlab;
+        r[k] = lut[lab * 256 + code];
+      }
+      *reinterpret_cast<float4*>(o + e0) = make_float4(r[0], r[1], r[2], r[3]);
+      *reinterpret_cast<float4*>(o + e0 + 4) = make_float4(r[4], r[5], r[6], r[7]);
+    }
+    e = c0 + nv * 8;
+  }
+  for (uint64_t i = e + threadIdx.x; i < c1; i += blockDim.x) {
+    const uint32_t lab = (ls[i / 2] >> (4 * (i & 1))) & 15u;
+    maxlab = lab > maxlab ? lab : maxlab;
+    o[i] = lut[lab * 256 + cs[i]];
+  }
+  // the reference raises with the largest label of the tensor (quantizer.py:196-197)
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) maxlab = max(maxlab, __shfl_xor_sync(kFull, maxlab, d));
+  if ((threadIdx.x & 31) == 0 && maxlab) atomicMax(&s_maxlab, maxlab);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_maxlab) {
+    atomicMax((unsigned long long*)&st->count, (unsigned long long)s_maxlab);
+    if (s_maxlab >= m) atomicOr(&st->err_flags, BSNP_ERR_LABEL);
+  }
+}
+
+// ------------------------------------------------------- precision report
+// sum (o-r)^2, sum |o-r|/|o| over |o| > 1e-12, count of such o (float64)
+__global__ void __launch_bounds__(kQThreads)
+    precision_kernel(const float* __restrict__ o, const float* __restrict__ r, uint64_t n,
+                     double* __restrict__ acc) {
+  double sse = 0.0, rel = 0.0, cnt = 0.0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const double a = (double)o[i], b = (double)r[i];
+    const double e = a - b;
+    sse += e * e;
+    if (fabs(a) > 1e-12) {
+      rel += fabs(e) / fabs(a);
+      cnt += 1.0;
+    }
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    sse += __shfl_xor_sync(kFull, sse, d);
+    rel += __shfl_xor_sync(kFull, rel, d);
+    cnt += __shfl_xor_sync(kFull, cnt, d);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&acc[0], sse);
+    atomicAdd(&acc[1], rel);
+    atomicAdd(&acc[2], cnt);
+  }
+}
+
+// ---------------------------------------------------------------- host plan
+uint32_t tree_depth(uint64_t len) {
+  std::vector<uint64_t> sizes{len};
+  uint32_t d = 0;
+  while (*std::max_element(sizes.begin(), sizes.end()) > kTileMax) {
+    std::vector<uint64_t> next;
+    for (uint64_t s : sizes) {
+      const uint64_t L = 8 * (s / 16);
+      next.push_back(L);
+      next.push_back(s - L);
+    }
+    std::sort(next.begin(), next.end());
+    next.erase(std::unique(next.begin(), next.end()), next.end());
+    sizes.swap(next);
+    ++d;
+  }
+  return d;
+}
+
+bool make_plan(uint64_t n, uint64_t block, int m, QPlan& P) {
+  if (n == 0) return false;
+  if (block != 0 && (block % 8) != 0) return false;
+  const uint64_t b = (block == 0 || block >= n) ? n : block;
+  P.n = n;
+  P.block = b;
+  P.nunits = (uint32_t)((n + b - 1) / b);
+  P.last_len = n - (uint64_t)(P.nunits - 1) * b;
+  P.m = (uint32_t)m;
+  P.D_full = tree_depth(b);
+  P.T_full = 1u << P.D_full;
+  P.D_last = tree_depth(P.last_len);
+  P.T_last = 1u << P.D_last;
+  P.total_tiles = (uint64_t)(P.nunits - 1) * P.T_full + P.T_last;
+  P.C_full = (uint32_t)((b + kDqChunk - 1) / kDqChunk);
+  P.C_last = (uint32_t)((P.last_len + kDqChunk - 1) / kDqChunk);
+  return true;
+}
+
+struct QWs {
+  double* partials;  // total_tiles
+  double* mu;        // nunits
+  float* fthr;       // nunits * 16
+  int* tile_mm;      // total_tiles * 32
+  size_t bytes;
+};
+
+QWs carve(const QPlan& P, void* ws) {
+  QWs w;
+  char* p = (char*)ws;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    char* r = p + o;
+    o = align_up(o + bytes, 256);
+    return r;
+  };
+  w.partials = (double*)take(8 * P.total_tiles);
+  w.mu = (double*)take(8 * (size_t)P.nunits);
+  w.fthr = (float*)take(64 * (size_t)P.nunits);
+  w.tile_mm = (int*)take(128 * P.total_tiles);
+  w.bytes = o;
+  return w;
+}
+
+int run_fit(const float* x, const QPlan& P, bsnp_cluster_table* tables, const QWs& w,
+            cudaStream_t s) {
+  int rc;
+  const unsigned tiles = (unsigned)P.total_tiles;
+  fit_tree_kernel<false><<<tiles, kQThreads, 0, s>>>(x, P, w.mu, w.partials);
+  if ((rc = launch_status("fit_tree_kernel<sum>"))) return rc;
+  fit_combine_kernel<false><<<P.nunits, kQThreads, 0, s>>>(P, w.partials, w.mu, w.fthr, tables);
+  if ((rc = launch_status("fit_combine_kernel<mean>"))) return rc;
+  fit_tree_kernel<true><<<tiles, kQThreads, 0, s>>>(x, P, w.mu, w.partials);
+  if ((rc = launch_status("fit_tree_kernel<var>"))) return rc;
+  fit_combine_kernel<true><<<P.nunits, kQThreads, 0, s>>>(P, w.partials, w.mu, w.fthr, tables);
+  if ((rc = launch_status("fit_combine_kernel<std>"))) return rc;
+  fit_minmax_kernel<<<tiles, kQThreads, 0, s>>>(x, P, w.fthr, w.tile_mm);
+  if ((rc = launch_status("fit_minmax_kernel"))) return rc;
+  fit_finalize_kernel<<<P.nunits, kQThreads, 0, s>>>(P, w.tile_mm, tables);
+  return launch_status("fit_finalize_kernel");
+}
+
+}  // namespace
+}  // namespace bsnp
+
+using namespace bsnp;
+
+extern "C" size_t bsnp_cluster_ws_bytes(uint64_t n, uint64_t block) {
+  QPlan P;
+  if (!make_plan(n ? n : 1, block, 16, P)) return 0;
+  return carve(P, nullptr).bytes;
+}
+
+extern "C" int bsnp_cluster_fit(const float* x, uint64_t n, uint64_t block, int m,
+                                bsnp_cluster_table* tables, void* ws, size_t ws_bytes,
+                                void* stream) {
+  QPlan P;
+  if (!x || !tables || !ws || m < 2 || m > 16 || !make_plan(n, block, m, P))
+    return BSNP_E_INVALID;
+  if (((uintptr_t)x & 3) || ((uintptr_t)tables & 15)) return BSNP_E_ALIGN;
+  const QWs w = carve(P, ws);
+  if (ws_bytes < w.bytes) return BSNP_E_WORKSPACE;
+  return run_fit(x, P, tables, w, (cudaStream_t)stream);
+}
+
+extern "C" int bsnp_cluster_quantize(const float* x, uint64_t n, uint64_t block,
+                                     const bsnp_cluster_table* tables, uint8_t* labels,
+                                     uint8_t* codes, void* ws, size_t ws_bytes, void* stream) {
+  QPlan P;
+  if (!x || !tables || !labels || !codes || !make_plan(n, block, 16, P)) return BSNP_E_INVALID;
+  if (((uintptr_t)x & 3) || ((uintptr_t)tables & 15)) return BSNP_E_ALIGN;
+  (void)ws;
+  (void)ws_bytes;
+  quantize_kernel<<<(unsigned)P.total_tiles, kQThreads, 0, (cudaStream_t)stream>>>(
+      x, P, tables, labels, codes);
+  return launch_status("quantize_kernel");
+}
+
+extern "C" int bsnp_cluster_encode(const float* x, uint64_t n, uint64_t block, int m,
+                                   bsnp_cluster_table* tables, uint8_t* labels, uint8_t* codes,
+                                   void* ws, size_t ws_bytes, void* stream) {
+  int rc = bsnp_cluster_fit(x, n, block, m, tables, ws, ws_bytes, stream);
+  if (rc) return rc;
+  return bsnp_cluster_quantize(x, n, block, tables, labels, codes, ws, ws_bytes, stream);
+}
+
+extern "C" int bsnp_cluster_dequantize(const uint8_t* labels, const uint8_t* codes, uint64_t n,
+                                       uint64_t block, const bsnp_cluster_table* tables,
+                                       float* out, bsnp_status* status, void* ws,
+                                       size_t ws_bytes, void* stream) {
+  QPlan P;
+  if (!labels || !codes || !tables || !out || !status || !make_plan(n, block, 16, P))
+    return BSNP_E_INVALID;
+  if (((uintptr_t)out & 3) || ((uintptr_t)tables & 15)) return BSNP_E_ALIGN;
+  (void)ws;
+  (void)ws_bytes;
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = cuda_status("memset(status)", cudaMemsetAsync(status, 0, sizeof(bsnp_status), s));
+  if (rc) return rc;
+  const uint64_t chunks = (uint64_t)(P.nunits - 1) * P.C_full + P.C_last;
+  dequantize_kernel<<<(unsigned)chunks, kQThreads, 0, s>>>(labels, codes, P, tables, out, status);
+  return launch_status("dequantize_kernel");
+}
+
+extern "C" int bsnp_precision_report(const float* original, const float* restored, uint64_t n,
+                                     double* acc3, void* stream) {
+  if (!acc3 || (n && (!original || !restored))) return BSNP_E_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = cuda_status("memset(acc)", cudaMemsetAsync(acc3, 0, 3 * sizeof(double), s));
+  if (rc || n == 0) return rc;
+  uint64_t grid = (n + kQThreads - 1) / kQThreads;
+  if (grid > 148 * 8) grid = 148 * 8;
+  precision_kernel<<<(unsigned)grid, kQThreads, 0, s>>>(original, restored, n, acc3);
+  return launch_status("precision_kernel");
+}
