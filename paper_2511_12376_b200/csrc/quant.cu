@@ -109,6 +109,60 @@ __device__ __forceinline__ uint32_t count_below(const float* t, float v) {
   return lo;
 }
 
+// Label lookup: #(bnd[k] < v) through a 64-bin uniform grid over
+// [bnd[0], bnd[m-2]]; each bin holds at most one boundary (else ok = 0 and
+// the 4-step binary search is used).  bin() is monotone in v and the table is
+// built with the same bin(), so the result is exact.
+struct LabelLut {
+  float g0, ginv;
+  uint32_t ok;
+  uint32_t ent[64];  // count of boundaries in lower bins | in-bin boundary index << 8
+  float bnd[16];     // +inf padded
+};
+
+__device__ __forceinline__ int lut_bin(float v, float g0, float ginv) {
+  const int b = __float2int_rd(__fmul_rn(__fsub_rn(v, g0), ginv));
+  return min(max(b, 0), 63);
+}
+
+__device__ __forceinline__ uint32_t lut_label(const LabelLut& L, float v) {
+  const uint32_t e = L.ent[lut_bin(v, L.g0, L.ginv)];
+  return (e & 0xffu) + (L.bnd[e >> 8] < v ? 1u : 0u);
+}
+
+__device__ __forceinline__ uint32_t label_of(const LabelLut& L, float v) {
+  return L.ok ? lut_label(L, v) : count_below(L.bnd, v);
+}
+
+// CTA-wide build of a label LUT (threads 0..63 build, all threads vote).
+// L.bnd[] (+inf padded) must be visible to every thread before the call.
+__device__ void lut_build_cta(LabelLut& L, int m) {
+  const int b = threadIdx.x;
+  const float g0 = L.bnd[0], g1 = L.bnd[m > 2 ? m - 2 : 0];
+  const float ginv = __fdiv_rn(64.0f, __fsub_rn(g1, g0));
+  const bool usable = m > 2 && g1 > g0 && isfinite(ginv) && ginv > 0.0f;
+  uint32_t cnt = 0;
+  if (b < 64) {
+    uint32_t base = 0, kin = 15;
+    for (int k = 0; k < m - 1; ++k) {
+      const int bk = lut_bin(L.bnd[k], g0, ginv);
+      if (bk < b) ++base;
+      else if (bk == b) {
+        kin = (uint32_t)k;
+        ++cnt;
+      }
+    }
+    L.ent[b] = base | (kin << 8);
+  }
+  const bool ok = __syncthreads_and(usable && cnt <= 1) != 0;
+  if (b == 0) {
+    L.g0 = g0;
+    L.ginv = ginv;
+    L.ok = ok ? 1u : 0u;
+  }
+  __syncthreads();
+}
+
 // Load elements [0, size) of a tile into padded shared memory.
 __device__ __forceinline__ void load_tile(float* s, const float* src, uint32_t size) {
   if (((uintptr_t)src & 15) == 0) {
@@ -207,6 +261,9 @@ __device__ double tree_sum(const float* s, uint32_t size, double mu, Heap& H) {
 
 // pass 1 / pass 2 of the fit: per-tile pairwise sums of x (kVar = false) or
 // of (x - mean)^2 (kVar = true)
+// perfect 8192-element tiles: 8 floats of padding per 1024 (8 leaves)
+__device__ __forceinline__ uint32_t epad(uint32_t e) { return e + ((e >> 10) << 3); }
+
 template <bool kVar>
 __global__ void __launch_bounds__(kQThreads)
     fit_tree_kernel(const float* __restrict__ x, QPlan P, const double* __restrict__ mu,
@@ -214,9 +271,46 @@ __global__ void __launch_bounds__(kQThreads)
   __shared__ __align__(16) float s[kSmemFloats];
   __shared__ Heap H;
   const TileRef r = locate(P, blockIdx.x);
-  load_tile(s, x + r.ustart + r.off, (uint32_t)r.size);
-  __syncthreads();
+  const float* src = x + r.ustart + r.off;
   const double m = kVar ? mu[r.u] : 0.0;
+  if (r.size == kTileMax && ((uintptr_t)src & 15) == 0) {
+    // a perfect sub-tree: 64 leaves of 128.  8 lanes per leaf (lane j owns
+    // numpy's accumulator r[j]); the 4 lane groups of a warp take leaves
+    // w, w+8, w+16, w+24 (+32), which the padding puts on distinct banks.
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t v = i * kQThreads + tid;
+      *reinterpret_cast<float4*>(&s[epad(4 * v)]) = ld_stream_f4(src + 4 * v);
+    }
+    __syncthreads();
+    const int j = lane & 7, q = lane >> 3;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int leaf = warp + 8 * q + 32 * h;
+      const float* lp = s + 128 * leaf + 8 * (leaf >> 3) + j;
+      float a[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) a[i] = lp[8 * i];
+      double acc = widen<kVar>(a[0], m);
+#pragma unroll
+      for (int i = 1; i < 16; ++i) acc = __dadd_rn(acc, widen<kVar>(a[i], m));
+      acc = __dadd_rn(acc, __shfl_xor_sync(kFull, acc, 1));
+      acc = __dadd_rn(acc, __shfl_xor_sync(kFull, acc, 2));
+      acc = __dadd_rn(acc, __shfl_xor_sync(kFull, acc, 4));
+      if (j == 0) H.val[leaf] = acc;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double v = __dadd_rn(H.val[2 * lane], H.val[2 * lane + 1]);
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) v = __dadd_rn(v, __shfl_xor_sync(kFull, v, d));
+      if (lane == 0) partials[blockIdx.x] = v;
+    }
+    return;
+  }
+  load_tile(s, src, (uint32_t)r.size);
+  __syncthreads();
   const double v = tree_sum<kVar>(s, (uint32_t)r.size, m, H);
   if (threadIdx.x == 0) partials[blockIdx.x] = v;
 }
@@ -303,45 +397,72 @@ __global__ void __launch_bounds__(kQThreads)
   for (int k = 0; k < 13; ++k) tb.reserved[k] = 0;
 }
 
-// pass 3 of the fit: per-tile, per-cluster min / max with fit-time labels
-__global__ void __launch_bounds__(kQThreads)
-    fit_minmax_kernel(const float* __restrict__ x, QPlan P, const float* __restrict__ fthr,
-                      int* __restrict__ tile_mm) {
-  __shared__ float thr[16];
-  __shared__ int smin[16], smax[16];
-  const TileRef r = locate(P, blockIdx.x);
-  const int tid = threadIdx.x;
-  if (tid < 16) {
-    thr[tid] = fthr[r.u * 16 + tid];
-    smin[tid] = 0x7fffffff;
-    smax[tid] = (int)0x80000000;
-  }
-  __syncthreads();
-  const float* src = x + r.ustart + r.off;
-  const uint32_t size = (uint32_t)r.size;
+template <bool kLut>
+__device__ __forceinline__ uint32_t label_t(const LabelLut& L, float v) {
+  return kLut ? lut_label(L, v) : count_below(L.bnd, v);
+}
+
+template <bool kLut>
+__device__ __forceinline__ void minmax_loop(const LabelLut& L, const float* src, uint32_t size,
+                                            int* mnrow, int* mxrow) {
+  const uint32_t mn_base = smem_addr(mnrow), mx_base = smem_addr(mxrow);
   auto visit = [&](float v) {
-    const uint32_t c = count_below(thr, v);
+    const uint32_t c = label_t<kLut>(L, v);
     const int k = fkey(v);
-    if (k < smin[c]) atomicMin(&smin[c], k);
-    if (k > smax[c]) atomicMax(&smax[c], k);
+    // predicated reductions: no branch / reconvergence per element; the
+    // read-compare filter keeps the (contended) atomics rare once extrema settle
+    asm volatile(
+        "{\n\t.reg .pred p, q;\n\t.reg .s32 a, b;\n\t"
+        "ld.shared.s32 a, [%0];\n\tld.shared.s32 b, [%1];\n\t"
+        "setp.lt.s32 p, %2, a;\n\tsetp.gt.s32 q, %2, b;\n\t"
+        "@p red.shared.min.s32 [%0], %2;\n\t@q red.shared.max.s32 [%1], %2;\n}" ::"r"(
+            mn_base + 4 * c),
+        "r"(mx_base + 4 * c), "r"(k)
+        : "memory");
   };
+  uint32_t done = 0;
   if (((uintptr_t)src & 15) == 0) {
     const uint32_t nv = size / 4;
-    for (uint32_t i = tid; i < nv; i += blockDim.x) {
+    for (uint32_t i = threadIdx.x; i < nv; i += kQThreads) {
       const float4 v = ld_stream_f4(src + 4 * i);
       visit(v.x);
       visit(v.y);
       visit(v.z);
       visit(v.w);
     }
-    for (uint32_t i = nv * 4 + tid; i < size; i += blockDim.x) visit(src[i]);
-  } else {
-    for (uint32_t i = tid; i < size; i += blockDim.x) visit(src[i]);
+    done = nv * 4;
+  }
+  for (uint32_t i = done + threadIdx.x; i < size; i += kQThreads) visit(src[i]);
+}
+
+// pass 3 of the fit: per-tile, per-cluster min / max with fit-time labels
+__global__ void __launch_bounds__(kQThreads)
+    fit_minmax_kernel(const float* __restrict__ x, QPlan P, const float* __restrict__ fthr,
+                      int* __restrict__ tile_mm) {
+  __shared__ LabelLut L;
+  __shared__ int wmin[kQThreads / 32][16], wmax[kQThreads / 32][16];
+  const TileRef r = locate(P, blockIdx.x);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < 16) L.bnd[tid] = fthr[r.u * 16 + tid];
+  if (lane < 16) {
+    wmin[warp][lane] = 0x7fffffff;
+    wmax[warp][lane] = (int)0x80000000;
   }
   __syncthreads();
+  lut_build_cta(L, (int)P.m);
+  const float* src = x + r.ustart + r.off;
+  const uint32_t size = (uint32_t)r.size;
+  if (L.ok) minmax_loop<true>(L, src, size, wmin[warp], wmax[warp]);
+  else minmax_loop<false>(L, src, size, wmin[warp], wmax[warp]);
+  __syncthreads();
   if (tid < 16) {
-    tile_mm[blockIdx.x * 32 + tid] = smin[tid];
-    tile_mm[blockIdx.x * 32 + 16 + tid] = smax[tid];
+    int a = 0x7fffffff, b = (int)0x80000000;
+    for (int w = 0; w < kQThreads / 32; ++w) {
+      a = min(a, wmin[w][tid]);
+      b = max(b, wmax[w][tid]);
+    }
+    tile_mm[blockIdx.x * 32 + tid] = a;
+    tile_mm[blockIdx.x * 32 + 16 + tid] = b;
   }
 }
 
@@ -438,30 +559,73 @@ __device__ __forceinline__ uint32_t quant_one(const QuantParams& Q, float v, uin
   return (uint32_t)e;
 }
 
+// code of one element from its cluster parameters; `amb` is set when the
+// float32 estimate is not provably exact (then exact_code decides)
+__device__ __forceinline__ uint32_t code_estimate(float v, float b, float rc, bool& amb) {
+  const float tt = __fsub_rn(__fmul_rn(__fsub_rn(v, b), rc), 0.5f);
+  amb |= !(fabsf(__fsub_rn(tt, rintf(tt))) > 0.000244140625f);  // also NaN
+  return (uint32_t)min(max(__float2int_ru(tt), 0), 255);
+}
+
+template <bool kLut>
+__device__ __forceinline__ void quant_loop(const LabelLut& L, const QuantParams& Q,
+                                           const float2* qp, const float* src, uint8_t* cdst,
+                                           uint8_t* ldst, uint32_t nv) {
+  for (uint32_t i = threadIdx.x; i < nv; i += kQThreads) {
+    const float4 v4 = ld_stream_f4(src + 4 * i);
+    const float v[4] = {v4.x, v4.y, v4.z, v4.w};
+    uint32_t c[4], code[4];
+    bool amb = false;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) c[e] = label_t<kLut>(L, v[e]);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 bp = qp[c[e]];
+      code[e] = code_estimate(v[e], bp.x, bp.y, amb);
+    }
+    if (__builtin_expect(amb, 0)) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        bool a1 = false;
+        code_estimate(v[e], qp[c[e]].x, qp[c[e]].y, a1);
+        if (a1) {
+          if (isnan(v[e])) c[e] = Q.last;
+          code[e] = exact_code(v[e], Q.off[c[e]], Q.scl[c[e]]);
+        }
+      }
+    }
+    *reinterpret_cast<uint32_t*>(cdst + 4 * i) =
+        code[0] | (code[1] << 8) | (code[2] << 16) | (code[3] << 24);
+    *reinterpret_cast<uint16_t*>(ldst + 2 * i) =
+        (uint16_t)(c[0] | (c[1] << 4) | (c[2] << 8) | (c[3] << 12));
+  }
+}
+
 __global__ void __launch_bounds__(kQThreads)
     quantize_kernel(const float* __restrict__ x, QPlan P,
                     const bsnp_cluster_table* __restrict__ tables, uint8_t* __restrict__ labels,
                     uint8_t* __restrict__ codes) {
   __shared__ QuantParams Q;
+  __shared__ LabelLut L;
+  __shared__ float2 qp[16];
   const TileRef r = locate(P, blockIdx.x);
   load_quant_params(tables[r.u], Q);
   __syncthreads();
+  if (threadIdx.x < 16) {
+    L.bnd[threadIdx.x] = Q.bnd[threadIdx.x];
+    qp[threadIdx.x] = make_float2(Q.off[threadIdx.x], Q.rcp[threadIdx.x]);
+  }
+  __syncthreads();
+  lut_build_cta(L, (int)tables[r.u].m);
   const float* src = x + r.ustart + r.off;
   uint8_t* cdst = codes + r.ustart + r.off;
   uint8_t* ldst = labels + (uint64_t)r.u * (P.block / 2) + r.off / 2;
   const uint32_t size = (uint32_t)r.size;
   const bool vec = (((uintptr_t)src & 15) | ((uintptr_t)cdst & 3) | ((uintptr_t)ldst & 1)) == 0;
   const uint32_t nv = vec ? size / 4 : 0;
-  for (uint32_t i = threadIdx.x; i < nv; i += blockDim.x) {
-    const float4 v = ld_stream_f4(src + 4 * i);
-    uint32_t l0, l1, l2, l3;
-    const uint32_t c0 = quant_one(Q, v.x, l0), c1 = quant_one(Q, v.y, l1);
-    const uint32_t c2 = quant_one(Q, v.z, l2), c3 = quant_one(Q, v.w, l3);
-    *reinterpret_cast<uint32_t*>(cdst + 4 * i) = c0 | (c1 << 8) | (c2 << 16) | (c3 << 24);
-    *reinterpret_cast<uint16_t*>(ldst + 2 * i) =
-        (uint16_t)((l0 | (l1 << 4)) | ((l2 | (l3 << 4)) << 8));
-  }
-  // tail (and unaligned tiles): element pairs
+  if (L.ok) quant_loop<true>(L, Q, qp, src, cdst, ldst, nv);
+  else quant_loop<false>(L, Q, qp, src, cdst, ldst, nv);
+  // tail (and unaligned tiles): element pairs through the reference-exact path
   for (uint32_t p = nv * 2 + threadIdx.x; 2 * p < size; p += blockDim.x) {
     uint32_t la, lb = 0;
     cdst[2 * p] = (uint8_t)quant_one(Q, src[2 * p], la);
@@ -689,27 +853,6 @@ __device__ __forceinline__ bool consumers_and(bool v) {
   return r != 0;
 }
 
-// Label lookup: #(bnd[k] < v) through a 64-bin uniform grid over
-// [bnd[0], bnd[m-2]]; each bin holds at most one boundary (else ok = 0 and
-// the 4-step binary search is used).  bin() is monotone in v and the table is
-// built with the same bin(), so the result is exact.
-struct LabelLut {
-  float g0, ginv;
-  uint32_t ok;
-  uint32_t ent[64];  // count of boundaries in lower bins | in-bin boundary index << 8
-  float bnd[16];     // +inf padded
-};
-
-__device__ __forceinline__ int lut_bin(float v, float g0, float ginv) {
-  const int b = __float2int_rd(__fmul_rn(__fsub_rn(v, g0), ginv));
-  return min(max(b, 0), 63);
-}
-
-__device__ __forceinline__ uint32_t lut_label(const LabelLut& L, float v) {
-  const uint32_t e = L.ent[lut_bin(v, L.g0, L.ginv)];
-  return (e & 0xffu) + (L.bnd[e >> 8] < v ? 1u : 0u);
-}
-
 // builder threads (b = 0..63) build one table (bnd[] already set); every
 // consumer thread calls it for the vote
 __device__ void lut_build(LabelLut& L, int m, int b, bool builder) {
@@ -736,9 +879,6 @@ __device__ void lut_build(LabelLut& L, int m, int b, bool builder) {
   }
 }
 
-__device__ __forceinline__ uint32_t label_of(const LabelLut& L, float v) {
-  return L.ok ? lut_label(L, v) : count_below(L.bnd, v);
-}
 
 // slot offset of tile element e: quarters are 8 floats apart in bank space
 __device__ __forceinline__ uint32_t qpad(uint32_t e) { return e + ((e / kQuarter) << 3); }
