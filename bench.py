@@ -316,7 +316,7 @@ def run_b200(args, rank: int, world: int, local_rank: int):
                      "frac": round(achieved / hbm, 4),
                      "algorithmic_bytes": dom_bytes,
                      "traffic": traffic},
-        "gpu_launches": 2 * args.steps,
+        "gpu_launches": 3 * args.steps,  # encode, offsets, decode per step
         "clocks": clk,
     }
     if e2e:
