@@ -48,6 +48,10 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-elems-per-core", type=int, default=1 << 23)
+    ap.add_argument("--no-c2", action="store_true",
+                    help="skip the C2 cluster-quantizer measurement")
+    ap.add_argument("--c2-log2n", type=int, default=30)
+    ap.add_argument("--c2-block", type=int, default=1 << 20)
     return ap.parse_args()
 
 
@@ -290,6 +294,8 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, base, cur, k, dev, world)
+    del base, cur, mask, payload, out
+    c2 = None if args.no_c2 else run_c2(args, dev, world)
 
     if rank != 0:
         return
@@ -321,9 +327,78 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     }
     if e2e:
         line["e2e"] = e2e
+    if c2:
+        line["c2_cluster_quant"] = c2
     if world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(args.p, args.cpu_elems_per_core)
     print(json.dumps(line), flush=True)
+
+
+def run_c2(args, dev, world):
+    """BASELINE configs[2] on the same GPU: 2^30 fp32 Adam-m-shaped state,
+    one cluster table per 2^20-element block, m = 16 (4-bit labels + u8
+    codes).  encode = build_clusters + quantize of every block,
+    decode = dequantize; both 5.5 bytes/element algorithmic."""
+    import torch
+    import torch.distributed as dist
+    from paper_2511_12376_b200 import quantizer as Q
+    from paper_2511_12376_b200 import _runtime as rt
+    n, block, m = 1 << args.c2_log2n, args.c2_block, 16
+    g = torch.Generator(device=dev).manual_seed(args.seed + 7)
+    x = torch.randn(n, device=dev, generator=g) * 1e-3
+    tables = Q.new_tables(n, block, dev)
+    labels = torch.empty(Q.unit_label_bytes(n, block), dtype=torch.uint8, device=dev)
+    codes = torch.empty(n, dtype=torch.uint8, device=dev)
+    out = torch.empty(n, dtype=torch.float32, device=dev)
+    st = rt.new_status(dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(max(3, args.warmup)):
+        Q.cluster_encode_async(x, m, block, tables, labels, codes)
+        Q.cluster_dequantize_async(labels, codes, n, block, tables, out, st)
+    torch.cuda.synchronize(dev)
+    (maxlab, flags), = rt.read_status(st)
+    assert flags == 0 and maxlab < m
+    err = float((out - x).abs().max())
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    if world > 1:
+        dist.barrier()
+    te = td = 0.0
+    for _ in range(args.steps):
+        ev[0].record(stream)
+        Q.cluster_encode_async(x, m, block, tables, labels, codes)
+        ev[1].record(stream)
+        Q.cluster_dequantize_async(labels, codes, n, block, tables, out, st)
+        ev[2].record(stream)
+        torch.cuda.synchronize(dev)
+        te += ev[0].elapsed_time(ev[1])
+        td += ev[1].elapsed_time(ev[2])
+    te /= args.steps
+    td /= args.steps
+    if world > 1:
+        t = torch.tensor([te, td], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        te, td = (float(v) for v in t.tolist())
+    units = Q.num_units(n, block)
+    algo = 4 * n + n + (n + 1) // 2            # read x, write codes + labels
+    enc_bytes = Q.serialized_quant_size("t", 1, block, m) * units
+    hbm, kind = peaks()
+    enc_gbs = world * algo / (te * 1e-3) / 1e9
+    dec_gbs = world * algo / (td * 1e-3) / 1e9
+    traffic = ncu_traffic().get("cluster_encode")
+    return {"workload": "C2: 2^%d fp32 ~N(0,1e-3), block %d, m=%d" % (args.c2_log2n, block, m),
+            "encode_ms": round(te, 4), "decode_ms": round(td, 4),
+            "encode_gbs": round(enc_gbs, 1), "decode_gbs": round(dec_gbs, 1),
+            "roofline_encode": {"bound": "hbm", "achieved": round(enc_gbs / world, 1),
+                                "peak": hbm, "peak_kind": kind, "unit": "GB/s",
+                                "frac": round(enc_gbs / world / hbm, 4),
+                                "algorithmic_bytes": algo, "traffic": traffic},
+            "roofline_decode": {"bound": "hbm", "achieved": round(dec_gbs / world, 1),
+                                "peak": hbm, "peak_kind": kind, "unit": "GB/s",
+                                "frac": round(dec_gbs / world / hbm, 4),
+                                "algorithmic_bytes": algo,
+                                "traffic": ncu_traffic().get("cluster_dequantize")},
+            "compression_ratio": round(4 * n / enc_bytes, 4),
+            "max_abs_err": err}
 
 
 def run_e2e(args, base, cur, k, dev, world):

@@ -109,3 +109,112 @@ def global_offsets(gathered: torch.Tensor, n_total: int):
     offsets = torch.cumsum(lengths, 0) - lengths
     return [(int(c), int(k), int(o), int(l))
             for c, k, o, l in zip(g[:, 1], g[:, 2], offsets, lengths)]
+
+
+# ---------------------------------------------------------------------------
+# sharded checkpoint encode (one process per GPU)
+# ---------------------------------------------------------------------------
+
+CODEC_CODES = {"RAW": CODEC_RAW, "DELTA": CODEC_DELTA, "QUANT": CODEC_QUANT}
+
+
+@dataclass(frozen=True)
+class TensorSpec:
+    """What every rank knows about every tensor (no data): enough to plan."""
+
+    name: str
+    group: str            # "model" | "optimizer"
+    nbytes: int
+
+
+def checkpoint_specs(ckpt) -> list:
+    return ([TensorSpec(t.name, "model", t.nbytes) for t in ckpt.model_states]
+            + [TensorSpec(t.name, "optimizer", t.nbytes) for t in ckpt.optimizer_states])
+
+
+@dataclass
+class ShardResult:
+    manifest: object            # store.CheckpointManifest, identical on every rank
+    records: list               # this rank's EncodedRecords
+    offsets: list               # their global offsets in tensors.bin
+    total_bytes: int            # length of the whole tensors.bin
+
+
+def encode_sharded(specs, local, prev_local, kind: str, iteration: int, base_iteration: int,
+                   rank: int, world: int, encoder, group=None, device=None,
+                   plan: ShardPlan | None = None) -> ShardResult:
+    """store.encode_checkpoint (store.py:214-272) across `world` ranks.
+
+    specs: [TensorSpec] of the whole checkpoint in checkpoint order (model
+    states, then optimizer states).  local: {name: tensor} holding at least
+    the tensors the plan assigns to this rank (TensorBlob or DeviceTensor);
+    prev_local: {name: previous model state} for those tensors (delta saves).
+    encoder: an object with `encode_records(items, prev_map, kind)` — the
+    store.CheckpointEncoder on a GPU.  The only communication is ONE
+    all-gather of (global_id, codec, count, encoded_bytes) rows; every rank
+    then derives the same manifest, whose offsets equal the single-process
+    driver's, so the records written at their offsets form a byte-identical
+    tensors.bin.
+    """
+    from .store import CheckpointManifest, ManifestEntry
+    if plan is None:
+        plan = plan_shards([s.nbytes for s in specs], world)
+    mine = plan.local_ids(rank)
+    items = [(gid, specs[gid].group, local[specs[gid].name]) for gid in mine]
+    prev_map = None
+    if kind == "delta":
+        prev_map = {specs[gid].name: prev_local[specs[gid].name]
+                    for gid in mine if specs[gid].group == "model"}
+    recs, _ = encoder.encode_records(items, prev_map, kind) if items else ([], {})
+    rows = [(r.gid, CODEC_CODES[r.codec], r.count, r.length) for r in recs]
+    gathered = exchange_sizes(rows, world, plan.max_rows, group=group, device=device)
+    table = global_offsets(gathered, len(specs))
+    names = {v: k for k, v in CODEC_CODES.items()}
+    entries = tuple(ManifestEntry(specs[i].name, specs[i].group, names[c], o, l)
+                    for i, (c, _, o, l) in enumerate(table))
+    manifest = CheckpointManifest(iteration=iteration, kind=kind,
+                                  base_iteration=base_iteration, tensors=entries)
+    total = (table[-1][2] + table[-1][3]) if table else 0
+    return ShardResult(manifest, recs, [table[r.gid][2] for r in recs], total)
+
+
+def write_shard(path: str, res: ShardResult, device=None) -> int:
+    """pwrite this rank's records at their global offsets of `path` (a
+    tensors.bin every rank opens; the file is sized to the full length).
+    Returns the bytes written."""
+    import os
+    import torch
+    from .store import sequential_offsets
+    local_offs = sequential_offsets(res.records)
+    buf = torch.empty(max(local_offs[-1], 1), dtype=torch.uint8,
+                      pin_memory=torch.cuda.is_available())
+    if res.records:
+        if device is None and torch.cuda.is_available():
+            device = torch.device("cuda", torch.cuda.current_device())
+        _place(res.records, local_offs, buf, device)
+    fd = os.open(path, os.O_WRONLY | os.O_CREAT, 0o644)
+    try:
+        if os.fstat(fd).st_size < res.total_bytes:
+            os.ftruncate(fd, res.total_bytes)
+        mv = memoryview(buf.numpy())
+        for r, lo, go in zip(res.records, local_offs, res.offsets):
+            os.pwrite(fd, mv[lo:lo + r.length], go)
+    finally:
+        os.close(fd)
+    return local_offs[-1]
+
+
+def _place(recs, offsets, buf, device):
+    from .store import place_records
+    if device is not None:
+        place_records(recs, offsets, buf, device)
+        return
+    # host-only records (CPU tests with a host encoder)
+    import numpy as np
+    b = buf.numpy()
+    for r, o in zip(recs, offsets):
+        b[o:o + len(r.header)] = np.frombuffer(r.header, np.uint8)
+        o += len(r.header)
+        for p in r.parts:
+            b[o:o + len(p)] = np.frombuffer(p, np.uint8)
+            o += len(p)

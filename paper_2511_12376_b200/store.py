@@ -1,0 +1,609 @@
+"""Checkpoint driver on the B200 codec: encode_checkpoint and chain replay.
+
+Drop-in for the codec half of /root/reference/pkg/src/bitsnap/store.py:
+  * `encode_checkpoint(ckpt, prev, kind, clusters)` (store.py:214-272): same
+    signature, same RAW/DELTA/QUANT decisions, same manifest and a
+    byte-identical `tensors.bin` blob;
+  * `decode_chain(chain)` (store.py:418-474 without the file system): replays
+    a base + delta chain of (manifest, tensors blob) pairs and dequantizes the
+    final optimizer states.
+
+What changes is where the work happens.  Every tensor of a checkpoint is
+encoded by sm_100a kernels (`_bsnp.so`) launched back to back on one stream
+into device arenas; the host learns every size (n_c per delta, the cluster
+tables) from ONE synchronisation, decides the codecs, assigns the offsets
+(store.py:240-247) and then lands headers and bodies straight at their final
+offsets of one pinned output buffer.  `CheckpointEncoder` additionally keeps
+the previous model states resident in HBM across saves (SURVEY §8(f) item 1:
+the service's decode-before-save, app.py:62-64, disappears), and
+`decode_chain` applies deltas in place on the device.
+
+The file-system lifecycle (tracker, commit, recovery, pruning) is out of scope
+(SURVEY §2); `write_tensors_bin` is the byte sink a store would call.
+"""
+
+from __future__ import annotations
+
+import json
+import struct
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import _runtime as rt
+from . import bitmask as B
+from . import quantizer as Q
+from .tensors import (ByteCursor, Checkpoint, ElementType, TENSOR_MAGIC, FORMAT_VERSION,
+                      TensorBlob, UnsupportedVersionError, tensor_header)
+
+KIND_BASE = "base"
+KIND_DELTA = "delta"
+CODEC_RAW = "RAW"
+CODEC_DELTA = "DELTA"
+CODEC_QUANT = "QUANT"
+GROUP_MODEL = "model"
+GROUP_OPTIMIZER = "optimizer"
+
+
+class StoreError(RuntimeError):
+    """store.py:66."""
+
+
+class MissingPreviousError(StoreError):
+    """store.py:79."""
+
+
+@dataclass(frozen=True)
+class ManifestEntry:
+    """store.py:124-130."""
+
+    name: str
+    group: str
+    codec: str
+    offset: int
+    length: int
+
+
+@dataclass(frozen=True)
+class CheckpointManifest:
+    """store.py:133-171 (same validation, byte-identical JSON)."""
+
+    iteration: int
+    kind: str
+    base_iteration: int
+    tensors: tuple = field(default_factory=tuple)
+
+    def __post_init__(self):
+        object.__setattr__(self, "tensors", tuple(self.tensors))
+        if self.kind not in (KIND_BASE, KIND_DELTA):
+            raise StoreError(f"unknown checkpoint kind {self.kind!r}")
+        if self.kind == KIND_DELTA and self.base_iteration >= self.iteration:
+            raise StoreError("delta checkpoint must reference an older base")
+        if self.kind == KIND_BASE and self.base_iteration != self.iteration:
+            raise StoreError("base checkpoint must reference itself")
+        for e in self.tensors:
+            if e.group == GROUP_MODEL and e.codec not in (CODEC_RAW, CODEC_DELTA):
+                raise StoreError(f"model tensor {e.name!r} has codec {e.codec}")
+            if e.group == GROUP_OPTIMIZER and e.codec not in (CODEC_QUANT, CODEC_RAW):
+                raise StoreError(f"optimizer tensor {e.name!r} has codec {e.codec}")
+
+    def to_bytes(self) -> bytes:
+        doc = {"iteration": self.iteration, "kind": self.kind,
+               "base_iteration": self.base_iteration,
+               "tensors": [vars(e) for e in self.tensors]}
+        return json.dumps(doc, separators=(",", ":")).encode("utf-8")
+
+    @classmethod
+    def from_bytes(cls, b: bytes) -> "CheckpointManifest":
+        try:
+            doc = json.loads(bytes(b).decode("utf-8"))
+            return cls(iteration=doc["iteration"], kind=doc["kind"],
+                       base_iteration=doc["base_iteration"],
+                       tensors=tuple(ManifestEntry(**e) for e in doc["tensors"]))
+        except (ValueError, KeyError, TypeError) as exc:
+            raise StoreError(f"corrupt manifest: {exc}") from exc
+
+
+# ---------------------------------------------------------------------------
+# device-resident tensors
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class DeviceTensor:
+    """A checkpoint tensor whose bytes live in HBM (the training process's own
+    parameter / optimizer buffers, no host copy).  `dtype` is the layout tag
+    (F16 for fp16 AND bf16 storage — SURVEY §8 N1, the bf16-ness travels out
+    of band in `data.dtype`)."""
+
+    name: str
+    dtype: ElementType
+    shape: tuple
+    data: torch.Tensor
+
+    def __post_init__(self):
+        object.__setattr__(self, "shape", tuple(int(s) for s in self.shape))
+        if self.data.element_size() != self.dtype.itemsize:
+            raise ValueError(f"tensor {self.name!r}: element size {self.data.element_size()} "
+                             f"does not match {self.dtype.name}")
+        if self.data.numel() != self.num_elements:
+            raise ValueError(f"tensor {self.name!r}: {self.data.numel()} elements, shape "
+                             f"{self.shape} requires {self.num_elements}")
+
+    @classmethod
+    def wrap(cls, name: str, t: torch.Tensor) -> "DeviceTensor":
+        if t.element_size() == 2:
+            dt = ElementType.F16
+        elif t.dtype == torch.float32:
+            dt = ElementType.F32
+        else:
+            raise ValueError(f"tensor {name!r}: unsupported dtype {t.dtype}")
+        return cls(name=name, dtype=dt, shape=tuple(t.shape), data=t)
+
+    @property
+    def num_elements(self) -> int:
+        n = 1
+        for s in self.shape:
+            n *= s
+        return n
+
+    @property
+    def nbytes(self) -> int:
+        return self.num_elements * self.dtype.itemsize
+
+    def flat(self) -> torch.Tensor:
+        d = self.data.reshape(-1)
+        if not d.is_contiguous():
+            d = d.contiguous()
+        return d.view(torch.int16 if self.dtype is ElementType.F16 else torch.float32)
+
+    def to_blob(self) -> TensorBlob:
+        return TensorBlob(name=self.name, dtype=self.dtype, shape=self.shape,
+                          data=rt.d2h_bytes(self.flat()))
+
+
+class _Uploader:
+    """Host TensorBlobs -> device tensors through one pinned staging buffer
+    (one host memcpy per tensor, async H2D copies, no per-tensor sync)."""
+
+    def __init__(self, device: torch.device, blobs):
+        self.dev = device
+        total = sum(b.nbytes for b in blobs)
+        self.stage = torch.empty(max(total, 1), dtype=torch.uint8, pin_memory=True)
+        self.np = self.stage.numpy()
+        self.off = 0
+
+    def put(self, blob: TensorBlob) -> torch.Tensor:
+        k = blob.nbytes
+        dt = torch.int16 if blob.dtype is ElementType.F16 else torch.float32
+        if k == 0:
+            return torch.empty(0, dtype=dt, device=self.dev)
+        s = self.np[self.off:self.off + k]
+        s[:] = np.frombuffer(blob.data, dtype=np.uint8)
+        out = torch.empty(k, dtype=torch.uint8, device=self.dev)
+        out.copy_(self.stage[self.off:self.off + k], non_blocking=True)
+        self.off += k
+        return out.view(dt)
+
+
+def _device_flat(t, up: _Uploader | None) -> torch.Tensor:
+    if isinstance(t, DeviceTensor):
+        return t.flat()
+    return up.put(t)
+
+
+# ---------------------------------------------------------------------------
+# encoded records
+# ---------------------------------------------------------------------------
+
+@dataclass
+class EncodedRecord:
+    """One tensor's encoded bytes, not yet placed: a host header followed by
+    body parts (device tensors, read back by D2H, or host byte views)."""
+
+    gid: int
+    name: str
+    group: str
+    codec: str
+    count: int                      # n_c (DELTA), m (QUANT), n (RAW)
+    header: bytes
+    parts: list
+
+    @property
+    def length(self) -> int:
+        return len(self.header) + sum(_part_nbytes(p) for p in self.parts)
+
+
+def _part_nbytes(p) -> int:
+    if isinstance(p, torch.Tensor):
+        return p.numel() * p.element_size()
+    return len(p)
+
+
+def _raw_record(gid, t, group, dev_flat) -> EncodedRecord:
+    body = t.data if isinstance(t, TensorBlob) else dev_flat
+    return EncodedRecord(gid, t.name, group, CODEC_RAW, t.num_elements,
+                         tensor_header(t.name, t.dtype, t.shape), [body])
+
+
+class CheckpointEncoder:
+    """encode_checkpoint (store.py:214-272) on one GPU.
+
+    `keep_prev=True` keeps the model states of the last encoded checkpoint
+    resident in HBM, so the next delta save needs no `prev` argument and no
+    host round trip of the previous checkpoint.
+    """
+
+    def __init__(self, device: torch.device | None = None, clusters: int = 16, block: int = 0,
+                 keep_prev: bool = True):
+        Q._check_m(clusters)
+        self.dev = rt.device_of() if device is None else torch.device(device)
+        self.clusters = clusters
+        self.block = block
+        self.keep_prev = keep_prev
+        self.prev = None            # (iteration, {name: device int16 flat tensor})
+
+    # -- phase 1 + 2: launch every codec, one sync, build unplaced records
+    def encode_records(self, items, prev_map, kind: str):
+        """items: [(gid, group, tensor)] in checkpoint order, tensor a
+        TensorBlob or DeviceTensor; prev_map: {name: tensor or device flat}.
+        Returns ([EncodedRecord], {name: device flat of the model states})."""
+        dev = self.dev
+        host = [t for _, _, t in items if isinstance(t, TensorBlob)]
+        host += [p for p in (prev_map or {}).values() if isinstance(p, TensorBlob)]
+        up = _Uploader(dev, host) if host else None
+        with torch.cuda.device(dev):
+            deltas, quants, model_dev = [], [], {}
+            n_mask = n_pay = n_lab = n_code = n_tab = 0
+            plan = []
+            for gid, group, t in items:
+                flat = _device_flat(t, up)
+                if group == GROUP_MODEL:
+                    model_dev[t.name] = flat
+                    if kind == KIND_DELTA:
+                        base = prev_map[t.name]
+                        if isinstance(base, TensorBlob):
+                            B._check_pair(base, t)
+                            bflat = up.put(base)
+                        else:
+                            bt = base if isinstance(base, DeviceTensor) else None
+                            if bt is not None:
+                                B._check_pair(bt, t)
+                                bflat = bt.flat()
+                            else:
+                                _check_pair_flat(t, base)
+                                bflat = base
+                        n = t.num_elements
+                        plan.append(("delta", gid, t, flat, bflat, n_mask, n_pay))
+                        n_mask += (n + 7) // 8
+                        n_pay += n
+                    else:
+                        plan.append(("raw", gid, t, flat))
+                else:
+                    if t.dtype is not ElementType.F32:
+                        raise Q.QuantizerError(f"tensor {t.name!r} is not F32")
+                    n = t.num_elements
+                    if n == 0:
+                        raise Q.QuantizerError(f"cannot cluster empty tensor {t.name!r}")
+                    plan.append(("quant", gid, t, flat, n_lab, n_code, n_tab))
+                    n_lab += Q.unit_label_bytes(n, self.block)
+                    n_code += n
+                    n_tab += Q.num_units(n, self.block)
+            mask_a = torch.empty(max(n_mask, 1), dtype=torch.uint8, device=dev)
+            pay_a = torch.empty(max(n_pay, 1), dtype=torch.int16, device=dev)
+            lab_a = torch.empty(max(n_lab, 1), dtype=torch.uint8, device=dev)
+            code_a = torch.empty(max(n_code, 1), dtype=torch.uint8, device=dev)
+            tab_a = torch.empty(max(n_tab, 1) * Q.TABLE_BYTES, dtype=torch.uint8, device=dev)
+            nd = sum(1 for p in plan if p[0] == "delta")
+            st = rt.new_status(dev, max(nd, 1))
+            di = 0
+            for p in plan:
+                if p[0] == "delta":
+                    _, gid, t, flat, bflat, mo, po = p
+                    n = t.num_elements
+                    if n:
+                        B.encode_delta_async(bflat, flat, mask_a[mo:mo + (n + 7) // 8],
+                                             pay_a[po:po + n], st[di])
+                    else:
+                        st[di].zero_()
+                    deltas.append((p, di))
+                    di += 1
+                elif p[0] == "quant":
+                    _, gid, t, flat, lo, co, to = p
+                    n = t.num_elements
+                    u = Q.num_units(n, self.block)
+                    Q.cluster_encode_async(flat, self.clusters, self.block,
+                                           tab_a[to * Q.TABLE_BYTES:(to + u) * Q.TABLE_BYTES],
+                                           lab_a[lo:lo + Q.unit_label_bytes(n, self.block)],
+                                           code_a[co:co + n])
+                    quants.append(p)
+            # the single synchronisation: every n_c and every cluster table
+            tab_h = torch.empty(tab_a.numel(), dtype=torch.uint8, pin_memory=True)
+            tab_h.copy_(tab_a, non_blocking=True)
+            status = rt.read_status(st)
+        tab_raw = tab_h.numpy().tobytes()
+        recs = {}
+        for (p, di) in deltas:
+            _, gid, t, flat, bflat, mo, po = p
+            n = t.num_elements
+            n_c, flags = status[di]
+            if flags & _lib.ERR_PAYLOAD_CAP:
+                raise B.DeltaError("internal: payload capacity exceeded")
+            raw_len = len(tensor_header(t.name, t.dtype, t.shape)) + 2 * n
+            dh = B.delta_header(t.name, t.shape, n, n_c)
+            if len(dh) + (n + 7) // 8 + 2 * n_c < raw_len:   # store.py:256
+                recs[gid] = EncodedRecord(gid, t.name, GROUP_MODEL, CODEC_DELTA, n_c, dh,
+                                          [mask_a[mo:mo + (n + 7) // 8], pay_a[po:po + n_c]])
+            else:
+                recs[gid] = _raw_record(gid, t, GROUP_MODEL, flat)
+        for p in plan:
+            if p[0] == "raw":
+                _, gid, t, flat = p
+                recs[gid] = _raw_record(gid, t, GROUP_MODEL, flat)
+        for p in quants:
+            _, gid, t, flat, lo, co, to = p
+            n = t.num_elements
+            u = Q.num_units(n, self.block)
+            tabs = [Q.ClusterTable.from_device_bytes(
+                tab_raw[(to + i) * Q.TABLE_BYTES:(to + i + 1) * Q.TABLE_BYTES]) for i in range(u)]
+            flags = [struct.unpack_from("<I", tab_raw, (to + i) * Q.TABLE_BYTES + 200)[0]
+                     for i in range(u)]
+            if any(f & _lib.ERR_NONFINITE for f in flags):
+                raise Q.QuantizerError(f"tensor {t.name!r} has non-finite values (NaN/Inf); "
+                                       "cluster statistics are undefined")
+            if u != 1:
+                raise StoreError("per-block quantization has no single-record BSQT layout; "
+                                 "use block=0 for store-compatible checkpoints")
+            recs[gid] = EncodedRecord(gid, t.name, GROUP_OPTIMIZER, CODEC_QUANT, self.clusters,
+                                      Q.quant_header(t.name, t.shape, tabs[0]),
+                                      [lab_a[lo:lo + (n + 1) // 2], code_a[co:co + n]])
+        return [recs[gid] for gid, _, _ in items], model_dev
+
+    # -- the reference entry point
+    def encode(self, ckpt: Checkpoint, prev: Checkpoint | None, kind: str):
+        """-> (CheckpointManifest, pinned uint8 tensor holding tensors.bin)."""
+        prev_map = self._prev_map(ckpt, prev, kind)
+        items = [(i, GROUP_MODEL, t) for i, t in enumerate(ckpt.model_states)]
+        k = len(items)
+        items += [(k + i, GROUP_OPTIMIZER, t) for i, t in enumerate(ckpt.optimizer_states)]
+        recs, model_dev = self.encode_records(items, prev_map, kind)
+        offsets = sequential_offsets(recs)
+        out = torch.empty(max(offsets[-1], 1), dtype=torch.uint8, pin_memory=True)[:offsets[-1]]
+        place_records(recs, offsets, out, self.dev)
+        base_iter = ckpt.iteration if kind == KIND_BASE else prev_iteration(prev, self.prev)
+        manifest = CheckpointManifest(
+            iteration=ckpt.iteration, kind=kind, base_iteration=base_iter,
+            tensors=tuple(ManifestEntry(r.name, r.group, r.codec, o, r.length)
+                          for r, o in zip(recs, offsets)))
+        if self.keep_prev:
+            # the device copies of host inputs become the next delta base;
+            # device-resident inputs are referenced (the caller owns them and
+            # must not mutate them before the next save, or pass prev)
+            self.prev = (ckpt.iteration, model_dev)
+        return manifest, out
+
+    def _prev_map(self, ckpt, prev, kind):
+        if kind not in (KIND_BASE, KIND_DELTA):
+            raise StoreError(f"unknown checkpoint kind {kind!r}")
+        if kind != KIND_DELTA:
+            return None
+        if prev is not None:
+            pm = {t.name: t for t in prev.model_states}
+        elif self.prev is not None:
+            pm = dict(self.prev[1])
+        else:
+            raise MissingPreviousError(
+                f"delta save at iteration {ckpt.iteration} needs the previous "
+                "reconstructed checkpoint")
+        if set(pm) != {t.name for t in ckpt.model_states}:
+            raise StoreError("model-state structure differs from previous checkpoint")
+        return pm
+
+
+def _check_pair_flat(t, base_flat: torch.Tensor) -> None:
+    if t.dtype is not ElementType.F16:
+        raise B.DeltaError("delta encoding requires F16 tensors")
+    if base_flat.numel() != t.num_elements:
+        raise B.DeltaError(f"shape mismatch for {t.name!r}: {base_flat.numel()} elements "
+                           f"vs {t.shape}")
+
+
+def prev_iteration(prev, resident) -> int:
+    if prev is not None:
+        return prev.iteration
+    return resident[0]
+
+
+def sequential_offsets(recs) -> list:
+    """store.py:240-247: offsets[i] = sum of the preceding lengths;
+    offsets[-1] = total."""
+    out, off = [], 0
+    for r in recs:
+        out.append(off)
+        off += r.length
+    out.append(off)
+    return out
+
+
+def place_records(recs, offsets, out: torch.Tensor, device: torch.device,
+                  base_offset: int = 0) -> None:
+    """Land every record at its offset of the pinned buffer `out` (headers by
+    host memcpy, device bodies by async D2H), then synchronise once."""
+    onp = out.numpy()
+    with torch.cuda.device(device):
+        for r, o in zip(recs, offsets):
+            o -= base_offset
+            h = len(r.header)
+            onp[o:o + h] = np.frombuffer(r.header, dtype=np.uint8)
+            o += h
+            for p in r.parts:
+                k = _part_nbytes(p)
+                if k == 0:
+                    continue
+                if isinstance(p, torch.Tensor):
+                    out[o:o + k].copy_(p.reshape(-1).view(torch.uint8), non_blocking=True)
+                else:
+                    onp[o:o + k] = np.frombuffer(p, dtype=np.uint8)
+                o += k
+        torch.cuda.current_stream(device).synchronize()
+
+
+def encode_checkpoint(ckpt: Checkpoint, prev: Checkpoint | None, kind: str,
+                      clusters: int = 16):
+    """store.py:214-272: -> (CheckpointManifest, bytes), byte-identical."""
+    enc = CheckpointEncoder(clusters=clusters, keep_prev=False)
+    manifest, out = enc.encode(ckpt, prev, kind)
+    return manifest, out.numpy().tobytes()
+
+
+# ---------------------------------------------------------------------------
+# load side: chain replay (store.py:418-474) over in-memory blobs
+# ---------------------------------------------------------------------------
+
+def _parse_raw(blob: memoryview, off: int):
+    cur = ByteCursor(blob[off:])
+    cur.magic(TENSOR_MAGIC)
+    (ver,) = cur.unpack("<H")
+    if ver != FORMAT_VERSION:
+        raise UnsupportedVersionError(f"unsupported format version {ver}")
+    (dt,) = cur.unpack("<B")
+    dtype = ElementType(dt)
+    name, shape = cur.name_and_shape()
+    n = 1
+    for s in shape:
+        n *= s
+    start = off + cur.pos
+    cur.take(n * dtype.itemsize)   # bounds check
+    return name, dtype, shape, start, n * dtype.itemsize
+
+
+def _parse_delta(blob: memoryview, off: int):
+    cur = ByteCursor(blob[off:])
+    cur.magic(B.DELTA_MAGIC)
+    (ver,) = cur.unpack("<H")
+    if ver != B.DELTA_VERSION:
+        raise B.DeltaError(f"unsupported delta version {ver}")
+    n, n_c = cur.unpack("<QQ")
+    name, shape = cur.name_and_shape()
+    mo = off + cur.pos
+    cur.take((n + 7) // 8)
+    po = off + cur.pos
+    cur.take(2 * n_c)
+    return name, shape, n, n_c, mo, po
+
+
+def decode_chain(chain, device: torch.device | None = None, to_host: bool = True):
+    """Reconstruct the last checkpoint of `chain` = [(manifest, tensors_blob)]
+    in ascending iteration order, the first being a base (store.py:429-474
+    after the manifests were read).  Model states are rebuilt on the device by
+    in-place delta application; optimizer states of the final manifest are
+    dequantized.  Returns a reference `Checkpoint` of TensorBlobs, or of
+    DeviceTensors with `to_host=False`."""
+    dev = rt.device_of() if device is None else torch.device(device)
+    if not chain or chain[0][0].kind != KIND_BASE:
+        raise StoreError("chain must start with a base checkpoint")
+    model: dict = {}
+    meta: dict = {}
+    model_order: list = []
+    final_opt = []
+    with torch.cuda.device(dev):
+        for ci, (manifest, blob) in enumerate(chain):
+            mv = memoryview(blob).cast("B")
+            pin = torch.empty(max(len(mv), 1), dtype=torch.uint8, pin_memory=True)
+            pin.numpy()[:len(mv)] = np.frombuffer(mv, dtype=np.uint8)
+            dblob = torch.empty(len(mv), dtype=torch.uint8, device=dev)
+            if len(mv):
+                dblob.copy_(pin[:len(mv)], non_blocking=True)
+            if manifest.kind == KIND_BASE:
+                model_order = []
+            checks = []
+            for e in manifest.tensors:
+                if e.group != GROUP_MODEL:
+                    continue
+                if e.codec == CODEC_RAW:
+                    name, dtype, shape, bo, k = _parse_raw(mv, e.offset)
+                    dt = torch.int16 if dtype is ElementType.F16 else torch.float32
+                    model[name] = dblob[bo:bo + k].clone().view(dt)
+                    meta[name] = (dtype, shape)
+                else:
+                    name, shape, n, n_c, mo, po = _parse_delta(mv, e.offset)
+                    if name not in model:
+                        raise KeyError(name)
+                    if meta[name][1] != shape:
+                        raise B.DeltaError(f"shape mismatch for {name!r}: "
+                                           f"{meta[name][1]} vs {shape}")
+                    base = model[name]
+                    if base.numel() != n:
+                        raise B.DeltaError("element count mismatch")
+                    if base.dtype != torch.int16:
+                        raise B.DeltaError("delta encoding requires F16 tensors")
+                    st = rt.new_status(dev)
+                    if n:
+                        pay = dblob[po:po + 2 * n_c]
+                        if po & 1:
+                            pay = pay.clone()
+                        B.decode_delta_async(base, dblob[mo:mo + (n + 7) // 8],
+                                             pay.view(torch.int16), n_c, base, st)
+                        checks.append((st, n_c))
+                    meta[name] = (ElementType.F16, shape)
+                if manifest.kind == KIND_BASE:
+                    model_order.append(e.name)
+            for st, n_c in checks:
+                (pc, flags), = rt.read_status(st)
+                B._raise_decode_flags(flags, pc, n_c)
+            if ci == len(chain) - 1:
+                for e in manifest.tensors:
+                    if e.group != GROUP_OPTIMIZER:
+                        continue
+                    if e.codec == CODEC_QUANT:
+                        final_opt.append(_dequant_entry(mv, dblob, e, dev))
+                    else:
+                        name, dtype, shape, bo, k = _parse_raw(mv, e.offset)
+                        dt = torch.int16 if dtype is ElementType.F16 else torch.float32
+                        final_opt.append((name, dtype, shape, dblob[bo:bo + k].clone().view(dt)))
+        if not model_order:
+            model_order = list(model)
+        final = chain[-1][0]
+        torch.cuda.current_stream(dev).synchronize()
+    ms = [DeviceTensor(nm, meta[nm][0], meta[nm][1], model[nm]) for nm in model_order]
+    os_ = [DeviceTensor(nm, dt, shp, t) for nm, dt, shp, t in final_opt]
+    if to_host:
+        ms = [t.to_blob() for t in ms]
+        os_ = [t.to_blob() for t in os_]
+    return Checkpoint(iteration=final.iteration, model_states=tuple(ms),
+                      optimizer_states=tuple(os_))
+
+
+def _dequant_entry(mv: memoryview, dblob: torch.Tensor, e: ManifestEntry, dev):
+    """BSQT record at e.offset -> dequantized device tensor; labels and codes
+    are read in place from the device copy of the blob."""
+    cur = ByteCursor(mv[e.offset:e.offset + e.length])
+    cur.magic(Q.QUANT_MAGIC)
+    (ver,) = cur.unpack("<H")
+    if ver != Q.QUANT_VERSION:
+        raise Q.QuantizerError(f"unsupported quantized-tensor version {ver}")
+    (m,) = cur.unpack("<B")
+    mean, std = cur.unpack("<ff")
+    table = Q.ClusterTable(m=m, mean=mean, std=std, boundaries=cur.unpack(f"<{m - 1}f"),
+                           scales=cur.unpack(f"<{m}f"), offsets=cur.unpack(f"<{m}f"))
+    name, shape = cur.name_and_shape()
+    n = 1
+    for s in shape:
+        n *= s
+    lo = e.offset + cur.pos
+    cur.take((n + 1) // 2)
+    co = e.offset + cur.pos
+    cur.take(n)
+    if n == 0:
+        return (name, ElementType.F32, shape, torch.empty(0, dtype=torch.float32, device=dev))
+    dq = Q.DeviceQuant(tables=rt.h2d_bytes(table.to_device_bytes(), dev),
+                       labels=dblob[lo:lo + (n + 1) // 2], codes=dblob[co:co + n],
+                       n=n, block=0, m=m)
+    return (name, ElementType.F32, shape, Q.cluster_dequantize_device(dq))
+
+
+def write_tensors_bin(path: str, blob) -> None:
+    """Byte sink of a store commit (store.py:350-351 writes tensors.bin)."""
+    with open(path, "wb") as f:
+        f.write(memoryview(blob.numpy() if isinstance(blob, torch.Tensor) else blob))

@@ -1,0 +1,232 @@
+"""Checkpoint driver on the GPU: encode_checkpoint (store.py:214-272) and the
+load-side chain replay (store.py:418-474) against the reference's own
+outputs (tests/golden/checkpoint_golden.npz, made by running the reference
+store) and the CPU oracle."""
+
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import bitsnap_oracle as O
+from paper_2511_12376_b200 import planner as P
+from paper_2511_12376_b200 import store as S
+from paper_2511_12376_b200.tensors import Checkpoint, ElementType, TensorBlob
+
+pytestmark = pytest.mark.gpu
+
+
+def _golden_ckpts(g, meta):
+    model0, model1, opt = [], [], []
+    for name, shape in meta["shapes"].items():
+        shape = tuple(shape)
+        model0.append(TensorBlob(name, ElementType.F16, shape, g[f"w0:{name}"].astype("<u2").tobytes()))
+        model1.append(TensorBlob(name, ElementType.F16, shape, g[f"w1:{name}"].astype("<u2").tobytes()))
+        for kind in ("m", "v"):
+            opt.append(TensorBlob(f"adam.{kind}.{name}", ElementType.F32, shape,
+                                  g[f"{kind}:{name}"].astype("<f4").tobytes()))
+    return (Checkpoint(iteration=100, model_states=model0, optimizer_states=opt),
+            Checkpoint(iteration=110, model_states=model1, optimizer_states=opt))
+
+
+def test_encode_checkpoint_matches_reference_golden(dev, checkpoint_golden, golden_index):
+    g, meta = checkpoint_golden, golden_index["checkpoint"]
+    c0, c1 = _golden_ckpts(g, meta)
+    man0, blob0 = S.encode_checkpoint(c0, None, S.KIND_BASE, 16)
+    man1, blob1 = S.encode_checkpoint(c1, c0, S.KIND_DELTA, 16)
+    assert blob0 == g["blob0"].tobytes()
+    assert blob1 == g["blob1"].tobytes()
+    assert man0.to_bytes() == g["manifest0"].tobytes()
+    assert man1.to_bytes() == g["manifest1"].tobytes()
+
+
+def test_resident_encoder_device_tensors(dev, checkpoint_golden, golden_index):
+    """Device-resident save path: DeviceTensors in, previous model states kept
+    in HBM between saves (no prev argument), same bytes as the reference."""
+    g, meta = checkpoint_golden, golden_index["checkpoint"]
+    c0, c1 = _golden_ckpts(g, meta)
+
+    def on_device(c, bf16):
+        wrap = []
+        for t in c.model_states:
+            a = torch.from_numpy(np.frombuffer(t.data, np.int16).copy()).to(dev)
+            wrap.append(S.DeviceTensor(t.name, t.dtype, t.shape,
+                                       a.view(torch.bfloat16) if bf16 else a))
+        opt = [S.DeviceTensor(t.name, t.dtype, t.shape,
+                              torch.from_numpy(np.frombuffer(t.data, np.float32).copy())
+                              .to(dev).reshape(t.shape)) for t in c.optimizer_states]
+        return Checkpoint(iteration=c.iteration, model_states=wrap, optimizer_states=opt)
+
+    enc = S.CheckpointEncoder(dev, clusters=16)
+    d0 = on_device(c0, bf16=True)
+    man0, out0 = enc.encode(d0, None, S.KIND_BASE)
+    man1, out1 = enc.encode(on_device(c1, bf16=True), None, S.KIND_DELTA)
+    assert out0.numpy().tobytes() == g["blob0"].tobytes()
+    assert out1.numpy().tobytes() == g["blob1"].tobytes()
+    assert man1.to_bytes() == g["manifest1"].tobytes()
+    assert man1.base_iteration == 100
+
+
+def test_decode_chain_round_trip(dev, checkpoint_golden, golden_index):
+    g, meta = checkpoint_golden, golden_index["checkpoint"]
+    c0, c1 = _golden_ckpts(g, meta)
+    chain = [(S.CheckpointManifest.from_bytes(g["manifest0"].tobytes()), g["blob0"].tobytes()),
+             (S.CheckpointManifest.from_bytes(g["manifest1"].tobytes()), g["blob1"].tobytes())]
+    out = S.decode_chain(chain)
+    assert out.iteration == 110
+    assert [t.name for t in out.model_states] == [t.name for t in c1.model_states]
+    for a, b in zip(out.model_states, c1.model_states):
+        assert a.data == b.data and a.shape == b.shape and a.dtype is ElementType.F16
+    for a, b in zip(out.optimizer_states, c1.optimizer_states):
+        x = np.frombuffer(b.data, np.float32)
+        tab = O.cluster_fit(x, 16)
+        p, c, _ = O.cluster_quantize(x, tab)
+        want = O.cluster_dequantize(p, c, x.size, tab)
+        assert a.data == want.astype("<f4").tobytes()
+    # base alone
+    out0 = S.decode_chain(chain[:1])
+    for a, b in zip(out0.model_states, c0.model_states):
+        assert a.data == b.data
+
+
+def _random_ckpt(rng, iteration, prev=None):
+    shapes = [(1000, 3), (8191,), (5,), (64, 64), (1,), (0,), (3, 3, 3)]
+    model = []
+    for i, shp in enumerate(shapes):
+        n = int(np.prod(shp))
+        if prev is None:
+            a = rng.integers(0, 1 << 16, n, dtype=np.uint16)
+        else:
+            a = np.frombuffer(prev.model_states[i].data, np.uint16).copy()
+            k = int(n * [0.01, 0.3, 1.0, 0.0, 1.0, 0, 0.5][i])
+            idx = rng.choice(n, k, replace=False) if k else np.zeros(0, np.int64)
+            a[idx] ^= rng.integers(1, 1 << 16, k, dtype=np.uint16)
+        model.append(TensorBlob(f"p{i}", ElementType.F16, shp, a.tobytes()))
+    opt = [TensorBlob(f"o{i}", ElementType.F32, (n,),
+                      (rng.standard_normal(n) * s).astype(np.float32).tobytes())
+           for i, (n, s) in enumerate([(3000, 1e-3), (1, 1.0), (129, 5.0), (70000, 1e-6)])]
+    return Checkpoint(iteration=iteration, model_states=model, optimizer_states=opt)
+
+
+def _oracle(ck, prev, kind, clusters=16):
+    conv = lambda ts, code: [(t.name, t.shape, code,
+                              np.frombuffer(t.data, np.uint16 if code == 0 else np.float32))
+                             for t in ts]
+    return O.encode_checkpoint(conv(ck.model_states, 0), conv(ck.optimizer_states, 1),
+                               conv(prev.model_states, 0) if prev else None, kind, clusters)
+
+
+@pytest.mark.parametrize("clusters", [16, 5, 2])
+def test_random_chain_vs_oracle(dev, clusters):
+    rng = np.random.default_rng(clusters)
+    c0 = _random_ckpt(rng, 1)
+    c1 = _random_ckpt(rng, 2, c0)
+    c2 = _random_ckpt(rng, 3, c1)
+    enc = S.CheckpointEncoder(dev, clusters=clusters)
+    chain = []
+    for ck, prev, kind in ((c0, None, "base"), (c1, c0, "delta"), (c2, c1, "delta")):
+        man, out = enc.encode(ck, None, kind)      # prev resident on the device
+        entries, want = _oracle(ck, prev, kind, clusters)
+        assert out.numpy().tobytes() == want
+        assert [vars(e) for e in man.tensors] == entries
+        chain.append((man, out.numpy().tobytes()))
+    rec = S.decode_chain(chain)
+    for a, b in zip(rec.model_states, c2.model_states):
+        assert a.data == b.data
+
+
+def test_store_errors(dev):
+    rng = np.random.default_rng(5)
+    c0 = _random_ckpt(rng, 1)
+    c1 = _random_ckpt(rng, 2, c0)
+    with pytest.raises(S.MissingPreviousError):
+        S.encode_checkpoint(c1, None, S.KIND_DELTA)
+    other = Checkpoint(iteration=1, model_states=c0.model_states[:-1],
+                       optimizer_states=c0.optimizer_states)
+    with pytest.raises(S.StoreError, match="structure"):
+        S.encode_checkpoint(c1, other, S.KIND_DELTA)
+    with pytest.raises(S.StoreError, match="kind"):
+        S.encode_checkpoint(c0, None, "full")
+    # a corrupt delta record (padding bits) is rejected on replay
+    man0, b0 = S.encode_checkpoint(c0, None, S.KIND_BASE)
+    man1, b1 = S.encode_checkpoint(c1, c0, S.KIND_DELTA)
+    e = [x for x in man1.tensors if x.codec == "DELTA" and x.name == "p6"][0]
+    bad = bytearray(b1)
+    hdr = 4 + 2 + 8 + 8 + 2 + len("p6") + 1 + 8 * 3
+    n = 27
+    bad[e.offset + hdr + (n + 7) // 8 - 1] |= 0x80
+    from paper_2511_12376_b200.bitmask import DeltaError
+    with pytest.raises(DeltaError, match="padding"):
+        S.decode_chain([(man0, b0), (man1, bytes(bad))])
+
+
+def test_planner_world1_with_gpu_encoder(dev, tmp_path):
+    rng = np.random.default_rng(11)
+    c0 = _random_ckpt(rng, 1)
+    c1 = _random_ckpt(rng, 2, c0)
+    specs = P.checkpoint_specs(c1)
+    local = {t.name: t for t in c1.model_states + c1.optimizer_states}
+    res = P.encode_sharded(specs, local, {t.name: t for t in c0.model_states}, "delta",
+                           2, 1, 0, 1, S.CheckpointEncoder(dev, keep_prev=False))
+    path = str(tmp_path / "tensors.bin")
+    P.write_shard(path, res)
+    man, want = S.encode_checkpoint(c1, c0, S.KIND_DELTA)
+    assert open(path, "rb").read() == want
+    assert res.manifest.to_bytes() == man.to_bytes()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _gpu_worker(rank, world, port, path, q):
+    """Two ranks sharing cuda:0 (independent kernels, no cross-rank waits);
+    the size-table all-gather goes over gloo."""
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(11)
+        c0 = _random_ckpt(rng, 1)
+        c1 = _random_ckpt(rng, 2, c0)
+        specs = P.checkpoint_specs(c1)
+        plan = P.plan_shards([s.nbytes for s in specs], world)
+        mine = {specs[i].name for i in plan.local_ids(rank)}
+        local = {t.name: t for t in c1.model_states + c1.optimizer_states if t.name in mine}
+        prev = {t.name: t for t in c0.model_states if t.name in mine}
+        dev = torch.device("cuda:0")
+        res = P.encode_sharded(specs, local, prev, "delta", 2, 1, rank, world,
+                               S.CheckpointEncoder(dev, keep_prev=False),
+                               device=torch.device("cpu"))
+        P.write_shard(path, res, device=dev)
+        dist.barrier()
+        q.put(res.manifest.to_bytes())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_planner_two_ranks_one_gpu(dev, tmp_path):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    path = str(tmp_path / "tensors.bin")
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, path, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    mans = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    rng = np.random.default_rng(11)
+    c0 = _random_ckpt(rng, 1)
+    c1 = _random_ckpt(rng, 2, c0)
+    entries, want = _oracle(c1, c0, "delta")
+    assert open(path, "rb").read() == want
+    assert mans[0] == mans[1]
+    assert [vars(e) for e in S.CheckpointManifest.from_bytes(mans[0]).tensors] == entries
