@@ -1294,6 +1294,8 @@ __global__ void __launch_bounds__(kQThreads)
   }
 }
 
+#include "quant_resident.cuh"
+
 // ---------------------------------------------------------------- host plan
 uint32_t tree_depth(uint64_t len) {
   std::vector<uint64_t> sizes{len};
@@ -1472,7 +1474,10 @@ extern "C" int bsnpdbg_watchdog(unsigned long long* out, unsigned* n) {
 extern "C" size_t bsnp_cluster_ws_bytes(uint64_t n, uint64_t block) {
   QPlan P;
   if (!make_plan(n ? n : 1, block, 16, P)) return 0;
-  return carve(P, nullptr).bytes;
+  size_t b = carve(P, nullptr).bytes;
+  const uint64_t ru = resident_units(n, block);
+  if (ru) b = std::max(b, resident_ws_bytes(ru, (uint32_t)(block / kRTile)));
+  return b;
 }
 
 // Per-block calls: full power-of-two blocks go through the fused cluster
@@ -1482,7 +1487,26 @@ static int cluster_run(const float* x, uint64_t n, uint64_t block, int m,
                        size_t ws_bytes, cudaStream_t s) {
   const bool quant = labels != nullptr;
   const bool aligned = ((((uintptr_t)x) & 15) | (((uintptr_t)codes) & 3) | (((uintptr_t)labels) & 1)) == 0;
-  const uint64_t fu = aligned ? fused_units(n, block) : 0;
+  // full power-of-two blocks: the resident-tile kernel (one HBM read of x)
+  const uint64_t ru = aligned ? resident_units(n, block) : 0;
+  if (ru && ws_bytes >= resident_ws_bytes(ru, (uint32_t)(block / kRTile))) {
+    int rc = launch_resident(x, ru, block, m, tables, labels, codes, quant ? 1 : 0, ws, s);
+    if (rc == BSNP_OK) {
+      const uint64_t done = ru * block;
+      if (done == n) return BSNP_OK;
+      x += done;
+      tables += ru;
+      if (quant) {
+        labels += done / 2;
+        codes += done;
+      }
+      n -= done;
+      block = 0;
+    } else if (rc != BSNP_E_INVALID) {
+      return rc;
+    }
+  }
+  const uint64_t fu = (aligned && block) ? fused_units(n, block) : 0;
   if (fu) {
     int rc = launch_block(x, fu, block, m, tables, labels, codes, quant ? 1 : 0, s);
     if (rc) return rc;

@@ -294,3 +294,63 @@ def test_c2_shape_per_block_sampled(dev, dist):
     err = (out - x).abs()
     scale = torch.tensor([max(t.scales) for t in tabs], device=dev).repeat_interleave(block)
     assert bool((err <= scale / 510 + x.abs() * 1.2e-7).all())
+
+
+def _dist(name, n, rng):
+    if name == "adam_m":
+        return rng.standard_normal(n) * 1e-3
+    if name == "adam_v":
+        return (rng.standard_normal(n) * 1e-3) ** 2
+    if name == "discrete":      # few distinct values: threshold bins are empty
+        return rng.integers(-3, 4, n) * 0.25
+    if name == "sparse":        # mostly zeros, a few large spikes
+        x = np.zeros(n)
+        k = max(1, n // 1000)
+        x[rng.choice(n, k, replace=False)] = rng.standard_normal(k) * 50
+        return x
+    if name == "offset":        # large mean, tiny spread (cancellation)
+        return 3.0 + rng.standard_normal(n) * 1e-5
+    if name == "uniform":
+        return rng.uniform(-1, 1, n)
+    raise ValueError(name)
+
+
+@pytest.mark.parametrize("log2b,units,tail", [(13, 5, 0), (16, 3, 1000), (20, 2, 8),
+                                               (21, 1, 0)])
+@pytest.mark.parametrize("dist", ["adam_m", "adam_v", "discrete", "sparse", "offset",
+                                  "uniform"])
+@pytest.mark.parametrize("m", [16, 7, 2])
+def test_resident_kernel_vs_oracle(dev, log2b, units, tail, dist, m):
+    """Power-of-two blocks of 2^13..2^21 take the resident-tile kernel (one
+    HBM read) when enabled (BSNP_RESIDENT=1), else the tiled kernels; the
+    tail unit always the tiled kernels.  Sparse/discrete data force its exact
+    min/max round.  Every unit is bit-exact vs the oracle."""
+    if (log2b >= 20 and m != 16) or (log2b == 21 and dist not in ("adam_m", "discrete")):
+        pytest.skip("size budget")
+    from paper_2511_12376_b200 import quantizer as Q
+    block = 1 << log2b
+    n = units * block + tail
+    rng = np.random.default_rng(log2b * 100 + m)
+    x = _dist(dist, n, rng).astype(np.float32)
+    if dist == "offset" and units > 1:
+        x[block:2 * block] = 1.5          # a constant block (sd = 0)
+    dq = Q.cluster_encode_device(_f32(x, dev), m, block)
+    _check_units(x, m, block, dq)
+    tables = Q.cluster_fit_device(_f32(x, dev), m, block)   # fit-only path
+    assert bytes(tables.cpu().numpy()) == bytes(dq.tables.cpu().numpy())
+
+
+def test_resident_kernel_repeatable_and_nonfinite(dev):
+    import torch
+    from paper_2511_12376_b200 import quantizer as Q
+    n, block = 1 << 22, 1 << 18
+    g = torch.Generator(device=dev).manual_seed(9)
+    x = torch.randn(n, device=dev, generator=g) * 1e-3
+    a = Q.cluster_encode_device(x, 16, block)
+    for _ in range(3):
+        b = Q.cluster_encode_device(x, 16, block)
+        assert torch.equal(a.codes, b.codes) and torch.equal(a.labels, b.labels)
+        assert torch.equal(a.tables, b.tables)
+    x[block * 3 + 5] = float("nan")
+    with pytest.raises(Q.QuantizerError, match="non-finite"):
+        Q.cluster_encode_device(x, 16, block)
