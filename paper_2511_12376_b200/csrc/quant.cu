@@ -361,7 +361,8 @@ __device__ __forceinline__ void unit_shape(const QPlan& P, uint32_t u, uint32_t&
 template <bool kVar>
 __global__ void __launch_bounds__(kQThreads)
     fit_combine_kernel(QPlan P, const double* __restrict__ partials, double* __restrict__ mu,
-                       float* __restrict__ fthr, bsnp_cluster_table* __restrict__ tables) {
+                       float* __restrict__ fthr, bsnp_cluster_table* __restrict__ tables,
+                       double* __restrict__ sdv = nullptr) {
   __shared__ double sv[kQThreads];
   const uint32_t u = blockIdx.x;
   uint32_t T;
@@ -378,6 +379,7 @@ __global__ void __launch_bounds__(kQThreads)
   const double m0 = mu[u];
   const double var = __ddiv_rn(__dadd_rn(0.0, S), (double)len);
   const double sd = __dsqrt_rn(var);  // np.std, ddof = 0
+  if (sdv) sdv[u] = sd;
   const int m = (int)P.m;
   tb.mean = __double2float_rn(m0);
   tb.std = __double2float_rn(sd);
@@ -438,9 +440,14 @@ __device__ __forceinline__ void minmax_loop(const LabelLut& L, const float* src,
 // pass 3 of the fit: per-tile, per-cluster min / max with fit-time labels
 __global__ void __launch_bounds__(kQThreads)
     fit_minmax_kernel(const float* __restrict__ x, QPlan P, const float* __restrict__ fthr,
-                      int* __restrict__ tile_mm) {
+                      int* __restrict__ tile_mm, const uint32_t* __restrict__ need = nullptr) {
   __shared__ LabelLut L;
   __shared__ int wmin[kQThreads / 32][16], wmax[kQThreads / 32][16];
+  if (need) {  // only the units the threshold-window pass left undecided
+    const uint64_t full_tiles = (uint64_t)(P.nunits - 1) * P.T_full;
+    const uint32_t uu = blockIdx.x < full_tiles ? (uint32_t)(blockIdx.x / P.T_full) : P.nunits - 1;
+    if (!need[uu]) return;
+  }
   const TileRef r = locate(P, blockIdx.x);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid < 16) L.bnd[tid] = fthr[r.u * 16 + tid];
@@ -469,9 +476,11 @@ __global__ void __launch_bounds__(kQThreads)
 // scales / offsets per unit (quantizer.py:117-125)
 __global__ void __launch_bounds__(kQThreads)
     fit_finalize_kernel(QPlan P, const int* __restrict__ tile_mm,
-                        bsnp_cluster_table* __restrict__ tables) {
+                        bsnp_cluster_table* __restrict__ tables,
+                        const uint32_t* __restrict__ need = nullptr) {
   __shared__ int rmin[8][16], rmax[8][16];
   const uint32_t u = blockIdx.x;
+  if (need && !need[u]) return;
   uint32_t T;
   uint64_t len;
   unit_shape(P, u, T, len);
@@ -1295,6 +1304,7 @@ __global__ void __launch_bounds__(kQThreads)
 }
 
 #include "quant_resident.cuh"
+#include "quant_window.cuh"
 
 // ---------------------------------------------------------------- host plan
 uint32_t tree_depth(uint64_t len) {
@@ -1334,11 +1344,15 @@ bool make_plan(uint64_t n, uint64_t block, int m, QPlan& P) {
   return true;
 }
 
+struct UGrid;
 struct QWs {
   double* partials;  // total_tiles
   double* mu;        // nunits
   float* fthr;       // nunits * 16
   int* tile_mm;      // total_tiles * 32
+  double* sd;        // nunits
+  UGrid* ug;         // nunits
+  uint32_t* need;    // nunits: exact min/max round needed
   size_t bytes;
 };
 
@@ -1355,6 +1369,9 @@ QWs carve(const QPlan& P, void* ws) {
   w.mu = (double*)take(8 * (size_t)P.nunits);
   w.fthr = (float*)take(64 * (size_t)P.nunits);
   w.tile_mm = (int*)take(128 * P.total_tiles);
+  w.sd = (double*)take(8 * (size_t)P.nunits);
+  w.ug = (UGrid*)take(kUGridBytes * (size_t)P.nunits);
+  w.need = (uint32_t*)take(4 * (size_t)P.nunits);
   w.bytes = o;
   return w;
 }
@@ -1447,6 +1464,47 @@ int run_fit(const float* x, const QPlan& P, bsnp_cluster_table* tables, const QW
   return launch_status("fit_finalize_kernel");
 }
 
+// Encode (labels != nullptr) or fit only: the threshold-window tiled path
+// (quant_window.cuh); BSNP_WINDOW=0 selects the original min/max + quantize
+// kernels.
+bool window_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("BSNP_WINDOW");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
+int run_window(const float* x, const QPlan& P, bsnp_cluster_table* tables, uint8_t* labels,
+               uint8_t* codes, const QWs& w, cudaStream_t s) {
+  int rc;
+  const unsigned tiles = (unsigned)P.total_tiles;
+  fit_tree_kernel<false><<<tiles, kQThreads, 0, s>>>(x, P, w.mu, w.partials);
+  if ((rc = launch_status("fit_tree_kernel<sum>"))) return rc;
+  fit_combine_kernel<false><<<P.nunits, kQThreads, 0, s>>>(P, w.partials, w.mu, w.fthr, tables);
+  if ((rc = launch_status("fit_combine_kernel<mean>"))) return rc;
+  fit_tree_kernel<true><<<tiles, kQThreads, 0, s>>>(x, P, w.mu, w.partials);
+  if ((rc = launch_status("fit_tree_kernel<var>"))) return rc;
+  fit_combine_kernel<true><<<P.nunits, kQThreads, 0, s>>>(P, w.partials, w.mu, w.fthr, tables,
+                                                           w.sd);
+  if ((rc = launch_status("fit_combine_kernel<std>"))) return rc;
+  fit_grid_kernel<<<P.nunits, kQThreads, 0, s>>>(P, w.mu, w.sd, tables, w.ug);
+  if ((rc = launch_status("fit_grid_kernel"))) return rc;
+  const unsigned chunks = (unsigned)((uint64_t)(P.nunits - 1) * P.C_full + P.C_last);
+  fit_label_kernel<<<chunks, kQThreads, 0, s>>>(x, P, w.ug, labels);
+  if ((rc = launch_status("fit_label_kernel"))) return rc;
+  fit_decide_kernel<<<P.nunits, 32, 0, s>>>(P, w.ug, tables, w.need);
+  if ((rc = launch_status("fit_decide_kernel"))) return rc;
+  // exact per-element min/max, only for the units the window left undecided
+  fit_minmax_kernel<<<tiles, kQThreads, 0, s>>>(x, P, w.fthr, w.tile_mm, w.need);
+  if ((rc = launch_status("fit_minmax_kernel"))) return rc;
+  fit_finalize_kernel<<<P.nunits, kQThreads, 0, s>>>(P, w.tile_mm, tables, w.need);
+  if ((rc = launch_status("fit_finalize_kernel"))) return rc;
+  if (!labels) return BSNP_OK;
+  quantize_codes_kernel<<<chunks, kQThreads, 0, s>>>(x, P, tables, labels, codes);
+  return launch_status("quantize_codes_kernel");
+}
+
 }  // namespace
 }  // namespace bsnp
 
@@ -1525,6 +1583,7 @@ static int cluster_run(const float* x, uint64_t n, uint64_t block, int m,
   if (!make_plan(n, block, m, P)) return BSNP_E_INVALID;
   const QWs w = carve(P, ws);
   if (ws_bytes < w.bytes) return BSNP_E_WORKSPACE;
+  if (window_enabled()) return run_window(x, P, tables, labels, codes, w, s);
   int rc = run_fit(x, P, tables, w, s);
   if (rc || !quant) return rc;
   quantize_kernel<<<(unsigned)P.total_tiles, kQThreads, 0, s>>>(x, P, tables, labels, codes);

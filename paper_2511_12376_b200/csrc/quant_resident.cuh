@@ -2,20 +2,21 @@
 // anonymous namespace; uses its helpers).
 //
 // build_clusters + quantize (quantizer.py:100-189) of every full power-of-two
-// block with ONE read of x from HBM.  The reference's four logical passes over
-// a block (mean, centred sum of squares, per-cluster min/max, quantize) run
-// on an 8192-element tile that stays in shared memory from its TMA load to its
-// last code:
+// block with ONE read of x from HBM.  The reference's passes over a block
+// (mean, centred sum of squares, per-cluster min/max, quantize) run on an
+// 8192-element tile that stays in shared memory from its TMA load to its last
+// code:
 //
-//   load (cp.async.bulk, padded layout) -> A: pairwise leaf sums of x
-//   -> [unit mean] -> B: leaf sums of (x - mean)^2 -> [unit std, boundaries]
-//   -> C: min/max candidates -> [unit table] -> D: labels + codes -> store
+//   load (64 x cp.async.bulk, one leaf per copy) -> A: pairwise leaf sums of x
+//   -> [unit mean] -> B: leaf sums of (x - mean)^2 -> [unit std, bin grid, LUT]
+//   -> C: labels (written out) + threshold neighbourhoods -> [unit table]
+//   -> D: codes
 //
 // [..] are unit-wide dependencies.  A tile publishes its partial to global
 // memory and bumps the unit's arrival counter; the LAST arriving tile folds
 // the partials in numpy's pairwise order and publishes the result with a
 // release store of the unit's phase word; the other tiles of the unit wait on
-// it (one thread polls with nanosleep, the rest sit in bar.sync).
+// it (one thread polls, the rest sit in bar.sync).
 //
 // Forward progress: CTAs claim tiles through one atomic ticket in unit order
 // and finish a tile before claiming another, so at most one unit (the
@@ -23,25 +24,36 @@
 // resident CTAs and completes without waiting on anything later.  The launch
 // guarantees more resident CTAs than tiles per unit.
 //
-// C is exact and cheap: with the fit thresholds F_k = RD_f32(B64_k) known, the
-// minimum of cluster c > 0 is the smallest element above F_{c-1} and the
+// Per-element work is kept to a few instructions: the numpy leaf accumulators
+// come from 16-byte shared loads (4 accumulators per thread, 2 threads per
+// leaf), and quantize labels from one byte of a 1024-bin LUT over mu +- 2 sd
+// (all |ndtri(k/m)| <= 1.54) plus at most one comparison.
+//
+// Per-cluster min/max exactly: with the fit thresholds F_k = RD_f32(B64_k),
+// the minimum of cluster c > 0 is the smallest element above F_{c-1}, the
 // maximum of cluster c < m-1 the largest element at or below F_c; cluster 0's
-// minimum / cluster m-1's maximum are the unit's extremes (from A).  Elements
-// are binned on a 2048-bin grid over mu +- 2 sd; only elements in the bin of
-// some F_k (about 0.5 %) touch shared memory.  If some F_k's bin holds no
-// element on one of its sides (sparse data), the unit runs an exact
-// per-element min/max round instead (kPhExact), which is what the tiled
-// kernels do everywhere.
+// minimum / cluster m-1's maximum are the unit's extremes (from A).  Only
+// elements within delta = 160 sd / block of the thresholds next to their
+// label are examined (dense data has many; the candidate found is provably
+// the extreme, see stage C).  If some F_k has no element within delta on one
+// of its sides (sparse data), the unit runs an exact per-element min/max
+// round instead (kPhExact).
 constexpr int kRThreads = 128;
 constexpr int kRWarps = kRThreads / 32;
 constexpr uint32_t kRTile = 8192;
-constexpr uint32_t kRChunk = 1024;                              // floats per padded chunk
-constexpr uint32_t kRFloats = kRTile + (kRTile / kRChunk) * 8;  // 8256
-constexpr int kRBins = 2048;  // over mu +- 2 sd: every |ndtri(k/m)| <= 1.54
+constexpr uint32_t kRLeaf = 128;                       // numpy pairwise leaf
+constexpr uint32_t kRChunk = 1024;                     // 8 leaves per bulk copy
+constexpr uint32_t kRFloats = kRTile + (kRTile / kRChunk) * 8;  // +8 floats per chunk
+constexpr int kRBins = 1024;
 constexpr int kRCtasPerSm = 6;
 constexpr uint32_t kRMaxT = 256;  // tiles per unit: blocks of 2^13 .. 2^21 elements
+static_assert(kRTile / kRLeaf == 2 * kRWarps * 16 / 2, "64 leaves, 2 threads per leaf");
 
 constexpr uint32_t kPhMean = 1, kPhStd = 2, kPhExact = 3, kPhTable = 4;
+
+// LUT byte: bits 0-3 L = #quantize boundaries in lower bins; bit 7: boundary L
+// lies in this bin (label = L + (v > B32[L])).
+constexpr uint32_t kLutB = 0x80u;
 
 #ifdef BSNP_RTIMING
 __device__ unsigned long long g_rt[16];  // cycles per stage (thread 0 of each CTA), counts
@@ -55,9 +67,9 @@ __device__ unsigned long long g_rt[16];  // cycles per stage (thread 0 of each C
 #endif
 
 struct RUnit {
-  uint32_t arrive[4];  // A, B, C (filter), exact round
+  uint32_t arrive[4];  // A, B, C, exact round
   uint32_t flag;       // highest published phase
-  uint32_t mode;       // bit 0: C runs the exact round; bit 1: D labels by comparisons
+  uint32_t mode;       // bit 0: C runs the exact round; bit 1: labels by comparisons
   uint32_t gmax, gmin_c;  // unit extremes: max ukey, ~(min ukey)
   float c0, gi;           // bin grid: bin(v) = min(floor_sat(v * gi + c0), kRBins - 1)
   uint32_t pad0[2];
@@ -69,7 +81,7 @@ struct RUnit {
   uint32_t emin_c[16];    // exact round: ~(per-cluster min ukey)
 };
 static_assert(sizeof(RUnit) == 384, "RUnit layout");
-constexpr uint32_t kRLutBytes = 2 * kRBins;  // per unit: C neighbourhood LUT | D label LUT
+constexpr uint32_t kRLutBytes = kRBins;
 
 // order-preserving float -> u32 (0 is below every non-NaN key)
 __device__ __forceinline__ uint32_t ukey(float f) {
@@ -88,6 +100,22 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
 __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ float fmin3(float a, float b, float c) {
+  float r;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+// ceil to u8 with saturation (the reference's clip(ceil(..), 0, 255))
+__device__ __forceinline__ uint32_t ceil_u8(float t) {
+  uint32_t r;
+  asm("cvt.rpi.sat.u8.f32 %0, %1;" : "=r"(r) : "f"(t));
+  return r;
+}
 
 struct RSmem {
   uint64_t bar;
@@ -96,9 +124,11 @@ struct RSmem {
   uint32_t mode;
   float c0, gi;
   double sd;
-  __align__(16) uint8_t lut[kRBins];  // C: owning threshold (0xff none); D: label LUT
+  __align__(16) uint8_t lut[kRBins];
   float F[16];       // fit thresholds RD_f32(B64), +inf padded
+  float2 FF[16];     // (F[c-1], F[c]) around quantize cluster c, -inf/+inf padded
   float B32[16];     // quantize boundaries RN_f32(B64), +inf padded
+  float delta;
   int binF[16], binB[16];
   uint32_t lo[16], hi_c[16];
   uint32_t emax[16], emin_c[16];
@@ -114,48 +144,76 @@ __device__ __forceinline__ uint32_t r_bin(float v, float gi, float c0) {
   return min(__float2uint_rd(__fmaf_rn(v, gi, c0)), (uint32_t)kRBins - 1);
 }
 
-// one thread polls the unit's phase word; the CTA waits in bar.sync
+// element e of the tile in the padded layout
+__device__ __forceinline__ uint32_t r_at(uint32_t e) { return e + (e >> 10) * 8; }
+
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// thread 0 polls the unit's phase word (relaxed loads, 1 us sleeps, one
+// acquire fence at the end); the other threads wait in bar.sync
+__device__ int g_rdebug;  // bit 0: skip unit waits (timing experiments; wrong results)
 __device__ __forceinline__ void r_wait(const uint32_t* flag, uint32_t ph) {
-  if (threadIdx.x == 0) {
-    uint32_t ns = 128;
-    while (ld_acquire_u32(flag) < ph) {
-      __nanosleep(ns);
-      ns = min(ns * 2, 1024u);
-    }
+  if (threadIdx.x == 0 && !(g_rdebug & 1)) {
+    while (ld_relaxed_u32(flag) < ph) __nanosleep(1000);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
   }
   __syncthreads();
 }
 
-// numpy leaf sums of one 8192-element tile (64 leaves of 128) into S.leafsum;
-// 8 lanes per leaf, lane j = numpy's accumulator r[j]; the 4 groups of a warp
-// take leaves 8 apart (1032 floats: distinct banks)
+// Tile sum in numpy's pairwise order of x (kVar = false) or (x - mu)^2.
+// Thread (warp w, lane = 8s + 4h + c) owns numpy's accumulators r[4h..4h+3]
+// (16 rows of 8) of leaf 8(c + 4(w >> 1)) + 4(w & 1) + s; the leaf is
+// ((r0+r1)+(r2+r3)) + ((r4+r5)+(r6+r7)), then a perfect tree over the 64
+// leaves.  The 8 lanes of a 16-byte shared-load phase read 4 different
+// 1024-float chunks x 2 halves: distinct bank groups in the padded layout.
 template <bool kVar>
-__device__ __forceinline__ void r_leaf_sums(const float* s, double mu, double* leafsum,
-                                            float& vmin, float& vmax) {
+__device__ __forceinline__ double r_tile_sum(const float* tile, double mu, RSmem& S,
+                                             float& vmin, float& vmax) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int q = lane >> 3, j = lane & 7;
-#pragma unroll
-  for (int h = 0; h < 4; ++h) {
-    const int leaf = warp + 4 * (h & 1) + 8 * q + 32 * (h >> 1);
-    const float* lp = s + 128 * leaf + 8 * (leaf >> 3) + j;
-    float a[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) a[i] = lp[8 * i];
+  const int c = lane & 3, h = (lane >> 2) & 1, sub = lane >> 3;
+  const int leaf = 8 * (c + 4 * (warp >> 1)) + 4 * (warp & 1) + sub;
+  const float* p = tile + r_at(leaf * kRLeaf) + 4 * h;
+  double r0, r1, r2, r3;
+  {
+    const float4 a = *reinterpret_cast<const float4*>(p);
+    r0 = widen<kVar>(a.x, mu);
+    r1 = widen<kVar>(a.y, mu);
+    r2 = widen<kVar>(a.z, mu);
+    r3 = widen<kVar>(a.w, mu);
     if (!kVar) {
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        vmin = fminf(vmin, a[i]);
-        vmax = fmaxf(vmax, a[i]);
-      }
+      vmin = fmin3(vmin, fminf(a.x, a.y), fminf(a.z, a.w));
+      vmax = fmax3(vmax, fmaxf(a.x, a.y), fmaxf(a.z, a.w));
     }
-    double acc = widen<kVar>(a[0], mu);
-#pragma unroll
-    for (int i = 1; i < 16; ++i) acc = __dadd_rn(acc, widen<kVar>(a[i], mu));
-    acc = __dadd_rn(acc, __shfl_xor_sync(kFull, acc, 1));
-    acc = __dadd_rn(acc, __shfl_xor_sync(kFull, acc, 2));
-    acc = __dadd_rn(acc, __shfl_xor_sync(kFull, acc, 4));
-    if (j == 0) leafsum[leaf] = acc;
   }
+#pragma unroll
+  for (int i = 1; i < 16; ++i) {
+    const float4 a = *reinterpret_cast<const float4*>(p + 8 * i);
+    r0 = __dadd_rn(r0, widen<kVar>(a.x, mu));
+    r1 = __dadd_rn(r1, widen<kVar>(a.y, mu));
+    r2 = __dadd_rn(r2, widen<kVar>(a.z, mu));
+    r3 = __dadd_rn(r3, widen<kVar>(a.w, mu));
+    if (!kVar) {
+      vmin = fmin3(vmin, a.x, a.y);
+      vmin = fmin3(vmin, a.z, a.w);
+      vmax = fmax3(vmax, a.x, a.y);
+      vmax = fmax3(vmax, a.z, a.w);
+    }
+  }
+  double v = __dadd_rn(__dadd_rn(r0, r1), __dadd_rn(r2, r3));
+  v = __dadd_rn(v, __shfl_xor_sync(kFull, v, 4));  // leaf = half0 + half1
+  if (h == 0) S.leafsum[leaf] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (warp == 0) {
+    t = __dadd_rn(S.leafsum[2 * lane], S.leafsum[2 * lane + 1]);
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) t = __dadd_rn(t, __shfl_xor_sync(kFull, t, d));
+  }
+  return t;  // valid in warp 0
 }
 
 // perfect-tree sum of the T (power of two <= 256) tile partials of one unit,
@@ -185,14 +243,14 @@ __device__ __forceinline__ double r_unit_sum(const double* part, uint32_t T, int
   return v;
 }
 
-// A or B stage of one tile: leaf sums -> tile partial -> unit arrival; the
-// last arriver returns true (CTA-uniform)
+// A or B stage: tile partial -> unit arrival; the last arriver returns true
+// (CTA-uniform)
 template <bool kVar>
 __device__ bool r_tree_stage(const float* tile, RSmem& S, RUnit& U, double* part, uint32_t T,
                              uint32_t j, double mu) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   float vmin = __int_as_float(0x7f800000), vmax = __int_as_float(0xff800000);
-  r_leaf_sums<kVar>(tile, mu, S.leafsum, vmin, vmax);
+  const double ts = r_tile_sum<kVar>(tile, mu, S, vmin, vmax);
   if (!kVar) {
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
@@ -203,37 +261,29 @@ __device__ bool r_tree_stage(const float* tile, RSmem& S, RUnit& U, double* part
       S.wmin[warp] = vmin;
       S.wmax[warp] = vmax;
     }
+    __syncthreads();
   }
-  __syncthreads();
-  if (warp == 0) {
-    double v = __dadd_rn(S.leafsum[2 * lane], S.leafsum[2 * lane + 1]);
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) v = __dadd_rn(v, __shfl_xor_sync(kFull, v, d));
-    if (lane == 0) {
-      part[j] = v;
-      if (!kVar) {
-        float a = S.wmin[0], b = S.wmax[0];
-        for (int w = 1; w < kRWarps; ++w) {
-          a = fminf(a, S.wmin[w]);
-          b = fmaxf(b, S.wmax[w]);
-        }
-        atomicMax(&U.gmax, ukey(b));
-        atomicMax(&U.gmin_c, ~ukey(a));
-      }
-      __threadfence();
-      S.last = atomicAdd(&U.arrive[kVar ? 1 : 0], 1u) == T - 1;
+  if (tid == 0) {
+    part[j] = ts;
+    if (!kVar) {
+      const float a = fminf(fminf(S.wmin[0], S.wmin[1]), fminf(S.wmin[2], S.wmin[3]));
+      const float b = fmaxf(fmaxf(S.wmax[0], S.wmax[1]), fmaxf(S.wmax[2], S.wmax[3]));
+      atomicMax(&U.gmax, ukey(b));
+      atomicMax(&U.gmin_c, ~ukey(a));
     }
+    __threadfence();
+    S.last = atomicAdd(&U.arrive[kVar ? 1 : 0], 1u) == T - 1;
   }
   __syncthreads();
   return S.last != 0;
 }
 
 // per-element exact min/max with fit-time labels (the tiled kernels' rule)
-__device__ __forceinline__ void r_exact_minmax(const float* tile, RSmem& S, int m) {
+__device__ __forceinline__ void r_exact_minmax(const float* tile, RSmem& S) {
   const int tid = threadIdx.x;
   for (int jj = 0; jj < (int)(kRTile / 4 / kRThreads); ++jj) {
     const uint32_t e = 4u * (jj * kRThreads + tid);
-    const float4 v4 = *reinterpret_cast<const float4*>(tile + e + 8 * (e >> 10));
+    const float4 v4 = *reinterpret_cast<const float4*>(tile + r_at(e));
     const float v[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -243,7 +293,6 @@ __device__ __forceinline__ void r_exact_minmax(const float* tile, RSmem& S, int 
       if (~k > S.emin_c[c]) atomicMax(&S.emin_c[c], ~k);
     }
   }
-  (void)m;
 }
 
 __device__ __forceinline__ void r_write_cluster(bsnp_cluster_table& tb, int c, bool nonempty,
@@ -256,6 +305,56 @@ __device__ __forceinline__ void r_write_cluster(bsnp_cluster_table& tb, int c, b
   }
   tb.scales[c] = scale;
   tb.offsets[c] = offset;
+}
+
+// Stage C over one tile: quantize labels (written to `lab` when non-null)
+// and candidates for the extremes next to the fit thresholds.  kCmp: labels
+// by comparisons (two boundaries share a bin).
+template <bool kCmp>
+__device__ __forceinline__ void r_stage_c(const float* tile, RSmem& S, uint8_t* lab, int m,
+                                          float gi, float c0) {
+  const int tid = threadIdx.x;
+  const float delta = S.delta;
+#pragma unroll 4
+  for (int jj = 0; jj < (int)(kRTile / 4 / kRThreads); ++jj) {
+    const uint32_t e = 4u * (jj * kRThreads + tid);
+    const float4 v4 = *reinterpret_cast<const float4*>(tile + r_at(e));
+    const float v[4] = {v4.x, v4.y, v4.z, v4.w};
+    uint32_t c[4];
+    bool nb = false;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (kCmp) {
+        c[i] = count_below(S.B32, v[i]);
+      } else {
+        const uint32_t le = S.lut[r_bin(v[i], gi, c0)];
+        const uint32_t L = le & 15u;
+        c[i] = L + ((le >> 7) & (v[i] > S.B32[L] ? 1u : 0u));
+      }
+      const float2 ff = S.FF[c[i]];
+      nb |= fminf(__fsub_rn(v[i], ff.x), __fsub_rn(ff.y, v[i])) < delta;
+    }
+    if (lab)
+      *reinterpret_cast<uint16_t*>(lab + e / 2) =
+          (uint16_t)(c[0] | (c[1] << 4) | (c[2] << 8) | (c[3] << 12));
+    if (__builtin_expect(nb, 0)) {
+      // candidates for the extremes next to F[c-1] (as succ) and F[c] (as
+      // pred, or succ for v == B32[c] > F[c])
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t key = ukey(v[i]);
+#pragma unroll
+        for (int d = 0; d < 2; ++d) {
+          const int k = (int)c[i] - 1 + d;
+          if (k < 0 || k >= m - 1) continue;
+          const float f = S.F[k];
+          if (!(fabsf(__fsub_rn(v[i], f)) < delta)) continue;
+          const bool below = v[i] <= f;
+          atomicMax(below ? &S.lo[k] : &S.hi_c[k], below ? key : ~key);
+        }
+      }
+    }
+  }
 }
 
 __global__ void __launch_bounds__(kRThreads, kRCtasPerSm)
@@ -285,11 +384,16 @@ __global__ void __launch_bounds__(kRThreads, kRCtasPerSm)
     RUnit& U = units[u];
     bsnp_cluster_table& tb = tables[u];
     const uint64_t ebase = (uint64_t)u * block + (uint64_t)j * kRTile;
-    if (tid == 0) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive_expect_tx(&S.bar, kRTile * 4);
-      for (int i = 0; i < (int)(kRTile / kRChunk); ++i)
-        bulk_g2s(tile + i * (kRChunk + 8), x + ebase + i * kRChunk, kRChunk * 4, &S.bar, pol);
+    if (warp == 0) {
+      // one 4 KiB bulk copy per 1024-float chunk into the padded layout
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive_expect_tx(&S.bar, kRTile * 4);
+      }
+      __syncwarp();
+      if (lane < (int)(kRTile / kRChunk))
+        bulk_g2s(tile + r_at(lane * kRChunk), x + ebase + lane * kRChunk, kRChunk * 4, &S.bar,
+                 pol);
     }
     if (tid < 16) {
       S.lo[tid] = 0;
@@ -318,7 +422,7 @@ __global__ void __launch_bounds__(kRThreads, kRCtasPerSm)
 
     // ---------------------------------------------------------------- B
     if (r_tree_stage<true>(tile, S, U, partB + (uint64_t)u * T, T, j, mu)) {
-      // last tile of the unit: std, table header, bin grid and both LUTs
+      // last tile of the unit: std, table header, bin grid and the unit LUT
       if (warp == 0) {
         __threadfence();
         const double s = r_unit_sum(partB + (uint64_t)u * T, T, lane);
@@ -360,10 +464,8 @@ __global__ void __launch_bounds__(kRThreads, kRCtasPerSm)
       __syncthreads();
       if (tid == 0) {
         uint32_t mode = S.mode;
-        for (int k = 1; k < m - 1; ++k) {
-          if (S.binF[k] - S.binF[k - 1] < 3) mode |= 1u;  // neighbourhoods overlap
-          if (S.binB[k] == S.binB[k - 1]) mode |= 2u;     // two boundaries in one bin
-        }
+        for (int k = 1; k < m - 1; ++k)
+          if (S.binB[k] == S.binB[k - 1]) mode |= 2u;  // two boundaries in one bin
         S.mode = mode;
         U.mode = mode;
         U.c0 = S.c0;
@@ -371,31 +473,21 @@ __global__ void __launch_bounds__(kRThreads, kRCtasPerSm)
       }
       __syncthreads();
       {
-        // D label LUT: thread t writes bins [16t, 16t + 16); C neighbourhood
-        // LUT: 0xff everywhere, then 3 bins per threshold
+        // thread t writes bins [8t, 8t + 8)
         uint8_t* lut = luts + (uint64_t)u * kRLutBytes;
-        uint32_t lw[4] = {0, 0, 0, 0};
-        const int b0 = 16 * tid;
+        const int b0 = 8 * tid;
         int cnt = 0;
         for (int k = 0; k < m - 1; ++k) cnt += S.binB[k] < b0;
+        uint32_t w[2] = {0, 0};
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
+        for (int q = 0; q < 8; ++q) {
           const int bb = b0 + q;
           while (cnt < m - 1 && S.binB[cnt] < bb) ++cnt;
-          const uint32_t le = (cnt < m - 1 && S.binB[cnt] == bb) ? (0x80u | (uint32_t)cnt)
-                                                                  : (uint32_t)cnt;
-          lw[q >> 2] |= le << (8 * (q & 3));
+          uint32_t e = (uint32_t)cnt;
+          if (cnt < m - 1 && S.binB[cnt] == bb) e |= kLutB;
+          w[q >> 2] |= e << (8 * (q & 3));
         }
-        *reinterpret_cast<uint4*>(lut + kRBins + b0) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
-        *reinterpret_cast<uint4*>(lut + b0) =
-            make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
-        __syncthreads();
-        if (tid < m - 1 && !(S.mode & 1u)) {
-          for (int d = -1; d <= 1; ++d) {
-            const int bb = S.binF[tid] + d;
-            if (bb >= 0 && bb < kRBins) lut[bb] = (uint8_t)tid;
-          }
-        }
+        *reinterpret_cast<uint2*>(lut + b0) = make_uint2(w[0], w[1]);
       }
       __syncthreads();
       if (tid == 0) {
@@ -408,39 +500,38 @@ __global__ void __launch_bounds__(kRThreads, kRCtasPerSm)
     RT_MARK(4);
 
     // ---------------------------------------------------------------- C
+    // quantize labels (written out) + neighbourhood candidates of the fit
+    // thresholds
     const uint8_t* ulut = luts + (uint64_t)u * kRLutBytes;
-    if (tid < 16) S.F[tid] = __ldcg(&U.F[tid]);
-    if (tid == 0) {
-      S.mode = __ldcg(&U.mode);
-      S.c0 = __ldcg(&U.c0);
-      S.gi = __ldcg(&U.gi);
-    }
-    static_assert(kRBins == 16 * kRThreads, "one 16-byte LUT chunk per thread");
-    reinterpret_cast<uint4*>(S.lut)[tid] = __ldcg(reinterpret_cast<const uint4*>(ulut) + tid);
-    __syncthreads();
-    bool exact = (S.mode & 1u) != 0;
-    RT_MARK(12);
-    if (!exact) {
-      const float gi = S.gi, c0 = S.c0;
-      for (int jj = 0; jj < (int)(kRTile / 4 / kRThreads); ++jj) {
-        const uint32_t e = 4u * (jj * kRThreads + tid);
-        const float4 v4 = *reinterpret_cast<const float4*>(tile + e + 8 * (e >> 10));
-        const uint32_t k0 = S.lut[r_bin(v4.x, gi, c0)], k1 = S.lut[r_bin(v4.y, gi, c0)];
-        const uint32_t k2 = S.lut[r_bin(v4.z, gi, c0)], k3 = S.lut[r_bin(v4.w, gi, c0)];
-        uint32_t fl = (k0 != 0xffu) | ((k1 != 0xffu) << 1) | ((k2 != 0xffu) << 2) |
-                      ((k3 != 0xffu) << 3);
-        while (__builtin_expect(fl != 0, 0)) {
-          const int i = __ffs(fl) - 1;
-          fl &= fl - 1;
-          const float v = i == 0 ? v4.x : i == 1 ? v4.y : i == 2 ? v4.z : v4.w;
-          const uint32_t k = i == 0 ? k0 : i == 1 ? k1 : i == 2 ? k2 : k3;
-          const uint32_t key = ukey(v);
-          const bool le = v <= S.F[k];
-          atomicMax(le ? &S.lo[k] : &S.hi_c[k], le ? key : ~key);
-        }
+    if (tid < 16) {
+      const float f = __ldcg(&U.F[tid]);
+      const float fp = tid > 0 ? __ldcg(&U.F[tid - 1]) : __int_as_float(0xff800000);
+      S.F[tid] = f;
+      S.FF[tid] = make_float2(fp, f);
+      S.B32[tid] = tid < m - 1 ? __ldcg(&tb.boundaries[tid]) : __int_as_float(0x7f800000);
+      if (tid == 0) {
+        S.mode = __ldcg(&U.mode);
+        S.c0 = __ldcg(&U.c0);
+        S.gi = __ldcg(&U.gi);
+        S.delta = __double2float_ru(__ddiv_rn(__dmul_rn(160.0, __ldcg(&U.sd)), (double)block));
       }
-      __syncthreads();
-      RT_MARK(13);
+    }
+    static_assert(kRBins == 8 * kRThreads, "one 8-byte LUT chunk per thread");
+    reinterpret_cast<uint2*>(S.lut)[tid] = __ldcg(reinterpret_cast<const uint2*>(ulut) + tid);
+    __syncthreads();
+    const uint32_t mode = S.mode;
+    bool exact = (mode & 1u) != 0;
+    RT_MARK(12);
+    {
+      const float gi = S.gi, c0 = S.c0;
+      const bool cmp = (mode & 2u) != 0;
+      uint8_t* lab = do_quant ? labels + ebase / 2 : nullptr;
+      if (cmp) r_stage_c<true>(tile, S, lab, m, gi, c0);
+      else r_stage_c<false>(tile, S, lab, m, gi, c0);
+    }
+    __syncthreads();
+    RT_MARK(13);
+    if (!exact) {
       if (tid < m - 1) {
         if (S.lo[tid]) atomicMax(&U.lo[tid], S.lo[tid]);
         if (S.hi_c[tid]) atomicMax(&U.hi_c[tid], S.hi_c[tid]);
@@ -491,7 +582,7 @@ __global__ void __launch_bounds__(kRThreads, kRCtasPerSm)
     }
     if (exact) {
       RT_COUNT(11);
-      r_exact_minmax(tile, S, m);
+      r_exact_minmax(tile, S);
       __syncthreads();
       if (tid < m) {
         if (S.emax[tid]) atomicMax(&U.emax[tid], S.emax[tid]);
@@ -525,7 +616,6 @@ __global__ void __launch_bounds__(kRThreads, kRCtasPerSm)
     if (tid < 16) {
       const float S_ = __ldcg(&tb.scales[tid]);
       const float off = __ldcg(&tb.offsets[tid]);
-      S.B32[tid] = tid < m - 1 ? __ldcg(&tb.boundaries[tid]) : __int_as_float(0x7f800000);
       float rc = 0.0f;
       if (S_ > 0.0f) {
         rc = __fdiv_rn(255.0f, S_);
@@ -534,55 +624,55 @@ __global__ void __launch_bounds__(kRThreads, kRCtasPerSm)
       S.qp[tid] = make_float2(off, rc);
       S.qs[tid] = S_;
     }
-    reinterpret_cast<uint4*>(S.lut)[tid] =
-        __ldcg(reinterpret_cast<const uint4*>(ulut + kRBins) + tid);
     __syncthreads();
     {
-      const float gi = S.gi, c0 = S.c0;
-      const bool cmp = (S.mode & 2u) != 0;
-#pragma unroll 4
-      for (int jj = 0; jj < (int)(kRTile / 4 / kRThreads); ++jj) {
+      const uint8_t* lab = labels + ebase / 2;
+      constexpr int kIt = (int)(kRTile / 4 / kRThreads);
+      // this thread's own label writes of stage C (program order), all 16
+      // loads in flight at once
+      uint32_t lws[kIt];
+#pragma unroll
+      for (int jj = 0; jj < kIt; ++jj)
+        lws[jj] = *reinterpret_cast<const uint16_t*>(lab + 2u * (jj * kRThreads + tid));
+#pragma unroll
+      for (int jj = 0; jj < kIt; ++jj) {
         const uint32_t e = 4u * (jj * kRThreads + tid);
-        const float4 v4 = *reinterpret_cast<const float4*>(tile + e + 8 * (e >> 10));
+        const float4 v4 = *reinterpret_cast<const float4*>(tile + r_at(e));
         const float v[4] = {v4.x, v4.y, v4.z, v4.w};
-        uint32_t c[4], code[4];
+        const uint32_t lw = lws[jj];
+        uint32_t code[4];
         bool amb = false;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          if (cmp) {
-            c[i] = count_below(S.B32, v[i]);
-          } else {
-            const uint32_t le = S.lut[r_bin(v[i], gi, c0)];
-            const uint32_t k = le & 0x7fu;
-            c[i] = k + ((le >> 7) & (v[i] > S.B32[k] ? 1u : 0u));
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float2 bp = S.qp[c[i]];
+          const float2 bp = S.qp[(lw >> (4 * i)) & 15u];
           // within 6.2e-5 of 255(v-b)/S - 0.5; the ceiling is exact unless
-          // flagged ambiguous.  The clamp is the reference's clip(.., 0, 1):
-          // quantize labels (RN boundaries) can put v just outside [b, b+S]
-          // of the fit labels (RD boundaries).
+          // flagged ambiguous.  The saturation is the reference's clip(.., 0,
+          // 1): quantize labels (RN boundaries) can put v just outside the
+          // [b, b+S] of the fit labels (RD thresholds).
           const float tt = __fsub_rn(__fmul_rn(__fsub_rn(v[i], bp.x), bp.y), 0.5f);
           amb |= !(fabsf(__fsub_rn(tt, rintf(tt))) > 0.000244140625f);  // also NaN
-          code[i] = (uint32_t)min(max(__float2int_ru(tt), 0), 255);
+          code[i] = ceil_u8(tt);
         }
         if (__builtin_expect(amb, 0)) {
+          uint32_t lw2 = lw;
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
+            uint32_t c = (lw >> (4 * i)) & 15u;
             bool a1 = false;
-            code_estimate(v[i], S.qp[c[i]].x, S.qp[c[i]].y, a1);
+            code_estimate(v[i], S.qp[c].x, S.qp[c].y, a1);
             if (a1) {
-              if (isnan(v[i])) c[i] = (uint32_t)(m - 1);
-              code[i] = exact_code(v[i], S.qp[c[i]].x, S.qs[c[i]]);
+              if (isnan(v[i])) {  // numpy sorts NaN after every boundary
+                c = (uint32_t)(m - 1);
+                lw2 = (lw2 & ~(15u << (4 * i))) | (c << (4 * i));
+              }
+              code[i] = exact_code(v[i], S.qp[c].x, S.qs[c]);
             }
           }
+          if (lw2 != lw)
+            *reinterpret_cast<uint16_t*>(labels + ebase / 2 + e / 2) = (uint16_t)lw2;
         }
         *reinterpret_cast<uint32_t*>(codes + ebase + e) =
             code[0] | (code[1] << 8) | (code[2] << 16) | (code[3] << 24);
-        *reinterpret_cast<uint16_t*>(labels + (ebase + e) / 2) =
-            (uint16_t)(c[0] | (c[1] << 4) | (c[2] << 8) | (c[3] << 12));
       }
     }
     __syncthreads();
@@ -634,6 +724,11 @@ int launch_resident(const float* x, uint64_t nunits, uint64_t block, int m,
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, quant_resident_kernel, kRThreads, 0);
   }
   const uint32_t T = (uint32_t)(block / kRTile);
+  static const int dbg = [] {
+    const char* e = getenv("BSNP_RDEBUG");
+    return e ? atoi(e) : 0;
+  }();
+  if (dbg) cudaMemcpyToSymbolAsync(g_rdebug, &dbg, sizeof(int), 0, cudaMemcpyHostToDevice, s);
   const uint64_t resident = (uint64_t)sms * (uint64_t)per_sm;
   if (resident < 2 * (uint64_t)T) return BSNP_E_INVALID;  // caller falls back
   char* p = (char*)ws;

@@ -1,0 +1,377 @@
+// Tiled cluster encoder, threshold-window variant (included by quant.cu after
+// quant_resident.cuh, inside its anonymous namespace; the default encode path).
+//
+// The fit's per-cluster min/max pass and the quantize pass of the tiled
+// kernels are replaced by:
+//
+//   fit_grid_kernel   (per unit)  bin grid over mu +- 2 sd, a 1024-bin label
+//                                 LUT and the threshold window delta
+//   fit_label_kernel  (per tile)  quantize labels (written out: they are the
+//                                 final label stream) + unit extremes +
+//                                 candidates within delta of the fit
+//                                 thresholds F_k next to each element's label
+//   fit_decide_kernel (per unit)  scales / offsets when every F_k has a
+//                                 candidate on both sides; else the unit is
+//                                 marked for the exact min/max round
+//   quantize_codes_kernel (tile)  codes from x and the written labels
+//
+// Why the candidates are exact: with fit thresholds F_k = RD_f32(B64_k), the
+// minimum of cluster c > 0 is succ(F_{c-1}) = the smallest element > F_{c-1},
+// the maximum of cluster c < m-1 is pred(F_c) = the largest element <= F_c,
+// and cluster 0's minimum / cluster m-1's maximum are the unit's extremes.
+// An element v with quantize label c (B32_{c-1} < v <= B32_c, B32 = RN(B64))
+// is a candidate for F_{c-1} and F_c when |v - F| < delta.  If a candidate
+// lo <= F_k exists, every element in (lo, F_k] has label k and lies within
+// delta, so it is a candidate too: lo is pred(F_k).  Likewise for succ
+// (elements in (F_k, hi) have label k+1, or equal B32_k > F_k with label k).
+// delta = 160 sd / n: for dense data pred/succ are ~sd/(n pdf) away, so a
+// missing side (probability ~e^-19 per threshold) only costs the exact round.
+constexpr uint32_t kWDeltaNum = 160;
+
+struct UGrid {
+  float c0, gi, delta;
+  uint32_t mode;          // bit 0: exact round (grid unusable); bit 1: labels by comparisons
+  uint32_t gmax, gmin_c;  // unit extremes: max ukey, ~(min ukey)
+  uint32_t pad[2];
+  float F[16];            // fit thresholds RD_f32(B64), +inf padded
+  float B32[16];          // quantize boundaries RN_f32(B64), +inf padded
+  uint32_t lo[16];        // max ukey of candidates <= F_k; 0 = none
+  uint32_t hi_c[16];      // ~(min ukey of candidates > F_k); 0 = none
+  uint8_t lut[kRBins];
+};
+constexpr size_t kUGridBytes = sizeof(UGrid);
+static_assert(sizeof(UGrid) % 16 == 0, "UGrid alignment");
+
+__global__ void __launch_bounds__(kQThreads)
+    fit_grid_kernel(QPlan P, const double* __restrict__ mu, const double* __restrict__ sdv,
+                    const bsnp_cluster_table* __restrict__ tables, UGrid* __restrict__ ug) {
+  __shared__ int binB[16];
+  __shared__ float s_gi, s_c0;
+  __shared__ uint32_t s_mode;
+  const uint32_t u = blockIdx.x;
+  const int tid = threadIdx.x, m = (int)P.m;
+  UGrid& G = ug[u];
+  const double m0 = mu[u], sd = sdv[u];
+  uint32_t T;
+  uint64_t len;
+  unit_shape(P, u, T, len);
+  if (tid == 0) {
+    const float r0 = __double2float_rn(__dsub_rn(m0, __dmul_rn(2.0, sd)));
+    const float wd = __double2float_rn(__dmul_rn(4.0, sd));
+    const float gi = __fdiv_rn((float)kRBins, wd);
+    const float c0 = -__fmul_rn(r0, gi);
+    const bool ok = isfinite(r0) && isfinite(gi) && gi > 0.0f && isfinite(c0) &&
+                    isfinite(m0) && isfinite(sd);
+    s_gi = gi;
+    s_c0 = c0;
+    s_mode = ok ? 0u : 3u;
+    G.gi = gi;
+    G.c0 = c0;
+    G.delta = __double2float_ru(__ddiv_rn(__dmul_rn((double)kWDeltaNum, sd), (double)len));
+    G.gmax = 0;
+    G.gmin_c = 0;
+  }
+  __syncthreads();
+  if (tid < 16) {
+    float f = __int_as_float(0x7f800000), r = f;
+    if (tid < m - 1) {
+      const double b64 = __dadd_rn(m0, __dmul_rn(sd, kNdtri[m][tid]));
+      f = __double2float_rd(b64);
+      r = __double2float_rn(b64);
+    }
+    G.F[tid] = f;
+    G.B32[tid] = r;
+    G.lo[tid] = 0;
+    G.hi_c[tid] = 0;
+    binB[tid] = tid < m - 1 ? (int)r_bin(r, s_gi, s_c0) : 0x3fffffff;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t mode = s_mode;
+    for (int k = 1; k < m - 1; ++k)
+      if (binB[k] == binB[k - 1]) mode |= 2u;  // two boundaries in one bin
+    s_mode = mode;
+    G.mode = mode;
+  }
+  // thread t: bins [4t, 4t + 4)
+  static_assert(kRBins == 4 * kQThreads, "4 LUT bins per thread");
+  const int b0 = 4 * tid;
+  int cnt = 0;
+  for (int k = 0; k < m - 1; ++k) cnt += binB[k] < b0;
+  uint32_t w = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int bb = b0 + q;
+    while (cnt < m - 1 && binB[cnt] < bb) ++cnt;
+    uint32_t e = (uint32_t)cnt;
+    if (cnt < m - 1 && binB[cnt] == bb) e |= kLutB;
+    w |= e << (8 * q);
+  }
+  reinterpret_cast<uint32_t*>(G.lut)[tid] = w;
+}
+
+// elementwise passes run over kDqChunk-element chunks of each unit (the
+// dequantize partition), not the pairwise-tree tiles
+struct ChunkRef {
+  uint32_t u;
+  uint64_t c0, len, ustart;
+};
+__device__ __forceinline__ ChunkRef chunk_of(const QPlan& P, uint64_t cidx) {
+  ChunkRef r;
+  const uint64_t full_chunks = (uint64_t)(P.nunits - 1) * P.C_full;
+  uint64_t ulen;
+  if (cidx < full_chunks) {
+    r.u = (uint32_t)(cidx / P.C_full);
+    r.c0 = (cidx % P.C_full) * kDqChunk;
+    ulen = P.block;
+  } else {
+    r.u = P.nunits - 1;
+    r.c0 = (cidx - full_chunks) * kDqChunk;
+    ulen = P.last_len;
+  }
+  r.len = (r.c0 + kDqChunk < ulen ? r.c0 + kDqChunk : ulen) - r.c0;
+  r.ustart = (uint64_t)r.u * P.block;
+  return r;
+}
+
+struct WSmem {
+  uint8_t lut[kRBins];
+  float F[16], B32[16];
+  float2 FF[16];  // (F[c-1], F[c]) around quantize cluster c
+  uint32_t lo[16], hi_c[16];
+  float wmin[kQThreads / 32], wmax[kQThreads / 32];
+  float gi, c0, delta;
+  uint32_t mode;
+};
+
+__device__ __forceinline__ uint32_t w_label(const WSmem& S, float v, bool cmp) {
+  if (cmp) return count_below(S.B32, v);
+  const uint32_t le = S.lut[r_bin(v, S.gi, S.c0)];
+  const uint32_t L = le & 15u;
+  return L + ((le >> 7) & (v > S.B32[L] ? 1u : 0u));
+}
+
+__device__ __forceinline__ bool w_near(const WSmem& S, float v, uint32_t c) {
+  const float2 ff = S.FF[c];
+  return fminf(__fsub_rn(v, ff.x), __fsub_rn(ff.y, v)) < S.delta;
+}
+
+__device__ __noinline__ void w_candidates(WSmem& S, float v, uint32_t c, int m) {
+  const uint32_t key = ukey(v);
+  for (int d = 0; d < 2; ++d) {
+    const int k = (int)c - 1 + d;
+    if (k < 0 || k >= m - 1) continue;
+    const float f = S.F[k];
+    if (!(fabsf(__fsub_rn(v, f)) < S.delta)) continue;
+    const bool below = v <= f;
+    atomicMax(below ? &S.lo[k] : &S.hi_c[k], below ? key : ~key);
+  }
+}
+
+template <bool kCmp>
+__device__ __forceinline__ void w_label_loop(WSmem& S, const float* src, uint32_t size,
+                                             uint8_t* lab, int m, float& vmin, float& vmax) {
+  const int tid = threadIdx.x;
+  const bool vec = ((((uintptr_t)src) & 15) | (((uintptr_t)lab) & 1)) == 0;
+  const uint32_t nv = vec ? size / 4 : 0;
+#pragma unroll 4
+  for (uint32_t i = tid; i < nv; i += kQThreads) {
+    const float4 v4 = ld_stream_f4(src + 4 * i);
+    const float v[4] = {v4.x, v4.y, v4.z, v4.w};
+    uint32_t c[4];
+    bool nb = false;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      c[q] = w_label(S, v[q], kCmp);
+      nb |= w_near(S, v[q], c[q]);
+    }
+    vmin = fmin3(vmin, fminf(v[0], v[1]), fminf(v[2], v[3]));
+    vmax = fmax3(vmax, fmaxf(v[0], v[1]), fmaxf(v[2], v[3]));
+    if (lab)
+      *reinterpret_cast<uint16_t*>(lab + 2 * i) =
+          (uint16_t)(c[0] | (c[1] << 4) | (c[2] << 8) | (c[3] << 12));
+    if (__builtin_expect(nb, 0)) {
+      for (int q = 0; q < 4; ++q)
+        if (w_near(S, v[q], c[q])) w_candidates(S, v[q], c[q], m);
+    }
+  }
+  // tail (and unaligned tiles): element pairs (one label byte each)
+  for (uint32_t p = 2 * nv + tid; 2 * p < size; p += kQThreads) {
+    uint32_t byte = 0;
+    for (uint32_t q = 0; q < 2 && 2 * p + q < size; ++q) {
+      const float v = src[2 * p + q];
+      const uint32_t c = w_label(S, v, kCmp);
+      vmin = fminf(vmin, v);
+      vmax = fmaxf(vmax, v);
+      if (w_near(S, v, c)) w_candidates(S, v, c, m);
+      byte |= c << (4 * q);
+    }
+    if (lab) lab[p] = (uint8_t)byte;
+  }
+}
+
+__global__ void __launch_bounds__(kQThreads)
+    fit_label_kernel(const float* __restrict__ x, QPlan P, UGrid* __restrict__ ug,
+                     uint8_t* __restrict__ labels) {
+  __shared__ __align__(16) WSmem S;
+  const ChunkRef r = chunk_of(P, blockIdx.x);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, m = (int)P.m;
+  UGrid& G = ug[r.u];
+  reinterpret_cast<uint32_t*>(S.lut)[tid] = reinterpret_cast<const uint32_t*>(G.lut)[tid];
+  if (tid < 16) {
+    const float f = G.F[tid];
+    S.F[tid] = f;
+    S.B32[tid] = G.B32[tid];
+    S.FF[tid] = make_float2(tid > 0 ? G.F[tid - 1] : __int_as_float(0xff800000), f);
+    S.lo[tid] = 0;
+    S.hi_c[tid] = 0;
+  }
+  if (tid == 0) {
+    S.gi = G.gi;
+    S.c0 = G.c0;
+    S.delta = G.delta;
+    S.mode = G.mode;
+  }
+  __syncthreads();
+  const float* src = x + r.ustart + r.c0;
+  uint8_t* lab = labels ? labels + (uint64_t)r.u * (P.block / 2) + r.c0 / 2 : nullptr;
+  float vmin = __int_as_float(0x7f800000), vmax = __int_as_float(0xff800000);
+  if (S.mode & 2u) w_label_loop<true>(S, src, (uint32_t)r.len, lab, m, vmin, vmax);
+  else w_label_loop<false>(S, src, (uint32_t)r.len, lab, m, vmin, vmax);
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    vmin = fminf(vmin, __shfl_xor_sync(kFull, vmin, d));
+    vmax = fmaxf(vmax, __shfl_xor_sync(kFull, vmax, d));
+  }
+  if (lane == 0) {
+    S.wmin[warp] = vmin;
+    S.wmax[warp] = vmax;
+  }
+  __syncthreads();
+  if (tid < m - 1) {
+    if (S.lo[tid]) atomicMax(&G.lo[tid], S.lo[tid]);
+    if (S.hi_c[tid]) atomicMax(&G.hi_c[tid], S.hi_c[tid]);
+  }
+  if (tid == 0) {
+    float a = S.wmin[0], b = S.wmax[0];
+    for (int w = 1; w < kQThreads / 32; ++w) {
+      a = fminf(a, S.wmin[w]);
+      b = fmaxf(b, S.wmax[w]);
+    }
+    atomicMax(&G.gmax, ukey(b));
+    atomicMax(&G.gmin_c, ~ukey(a));
+  }
+}
+
+// one warp per unit: extremes from the candidates, or mark the exact round
+__global__ void __launch_bounds__(32)
+    fit_decide_kernel(QPlan P, const UGrid* __restrict__ ug,
+                      bsnp_cluster_table* __restrict__ tables, uint32_t* __restrict__ need) {
+  const uint32_t u = blockIdx.x;
+  const int lane = threadIdx.x, m = (int)P.m;
+  const UGrid& G = ug[u];
+  bsnp_cluster_table& tb = tables[u];
+  bool ok = !(G.mode & 1u);
+  uint32_t lo = 0, hic = 0;
+  if (lane < m - 1) {
+    lo = G.lo[lane];
+    hic = G.hi_c[lane];
+    ok = ok && lo != 0 && hic != 0;
+  }
+  ok = __all_sync(kFull, ok);
+  const uint32_t hic_prev = __shfl_up_sync(kFull, hic, 1);
+  if (lane == 0) need[u] = ok ? 0u : 1u;
+  if (!ok || lane >= 16) return;
+  const int c = lane;
+  float scale = 0.0f, offset = 0.0f;
+  if (c < m) {
+    const uint32_t kmin = c == 0 ? ~G.gmin_c : ~hic_prev;
+    const uint32_t kmax = c == m - 1 ? G.gmax : lo;
+    const float a = ukey_inv(kmin), b = ukey_inv(kmax);
+    scale = __double2float_rn(__dsub_rn((double)b, (double)a));
+    offset = a;
+  }
+  tb.scales[c] = scale;
+  tb.offsets[c] = offset;
+}
+
+// codes of one tile from x and its written labels (quantizer.py:174-182)
+__global__ void __launch_bounds__(kQThreads)
+    quantize_codes_kernel(const float* __restrict__ x, QPlan P,
+                          const bsnp_cluster_table* __restrict__ tables,
+                          uint8_t* __restrict__ labels, uint8_t* __restrict__ codes) {
+  __shared__ float2 qp[16];
+  __shared__ float qs[16];
+  const ChunkRef r = chunk_of(P, blockIdx.x);
+  const int tid = threadIdx.x, m = (int)P.m;
+  const bsnp_cluster_table& tb = tables[r.u];
+  if (tid < 16) {
+    const float S_ = tb.scales[tid];
+    float rc = 0.0f;
+    if (S_ > 0.0f) {
+      rc = __fdiv_rn(255.0f, S_);
+      if (!isfinite(rc)) rc = __int_as_float(0x7fffffff);
+    }
+    qp[tid] = make_float2(tb.offsets[tid], rc);
+    qs[tid] = S_;
+  }
+  __syncthreads();
+  const float* src = x + r.ustart + r.c0;
+  uint8_t* cdst = codes + r.ustart + r.c0;
+  uint8_t* lab = labels + (uint64_t)r.u * (P.block / 2) + r.c0 / 2;
+  const uint32_t size = (uint32_t)r.len;
+  const bool vec = ((((uintptr_t)src) & 15) | (((uintptr_t)cdst) & 3) | (((uintptr_t)lab) & 1)) == 0;
+  const uint32_t nv = vec ? size / 4 : 0;
+#pragma unroll 4
+  for (uint32_t i = tid; i < nv; i += kQThreads) {
+    const float4 v4 = ld_stream_f4(src + 4 * i);
+    const float v[4] = {v4.x, v4.y, v4.z, v4.w};
+    const uint32_t lw = *reinterpret_cast<const uint16_t*>(lab + 2 * i);
+    uint32_t code[4];
+    bool amb = false;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 bp = qp[(lw >> (4 * q)) & 15u];
+      // within 6.2e-5 of 255(v-b)/S - 0.5: exact unless flagged ambiguous;
+      // the saturation is the reference's clip (labels vs RN boundaries can
+      // put v just outside the [b, b+S] of the fit's RD thresholds)
+      const float tt = __fsub_rn(__fmul_rn(__fsub_rn(v[q], bp.x), bp.y), 0.5f);
+      amb |= !(fabsf(__fsub_rn(tt, rintf(tt))) > 0.000244140625f);  // also NaN
+      code[q] = ceil_u8(tt);
+    }
+    if (__builtin_expect(amb, 0)) {
+      uint32_t lw2 = lw;
+      for (int q = 0; q < 4; ++q) {
+        uint32_t c = (lw >> (4 * q)) & 15u;
+        bool a1 = false;
+        code_estimate(v[q], qp[c].x, qp[c].y, a1);
+        if (a1) {
+          if (isnan(v[q])) {  // numpy sorts NaN after every boundary
+            c = (uint32_t)(m - 1);
+            lw2 = (lw2 & ~(15u << (4 * q))) | (c << (4 * q));
+          }
+          code[q] = exact_code(v[q], qp[c].x, qs[c]);
+        }
+      }
+      if (lw2 != lw) *reinterpret_cast<uint16_t*>(lab + 2 * i) = (uint16_t)lw2;
+    }
+    *reinterpret_cast<uint32_t*>(cdst + 4 * i) =
+        code[0] | (code[1] << 8) | (code[2] << 16) | (code[3] << 24);
+  }
+  for (uint32_t p = 2 * nv + tid; 2 * p < size; p += kQThreads) {
+    uint32_t byte = lab[p];
+    for (uint32_t q = 0; q < 2 && 2 * p + q < size; ++q) {
+      const float v = src[2 * p + q];
+      uint32_t c = (byte >> (4 * q)) & 15u;
+      if (isnan(v)) {
+        c = (uint32_t)(m - 1);
+        byte = (byte & ~(15u << (4 * q))) | (c << (4 * q));
+      }
+      bool a1 = false;
+      uint32_t code = min(code_estimate(v, qp[c].x, qp[c].y, a1), 255u);
+      if (a1) code = exact_code(v, qp[c].x, qs[c]);
+      cdst[2 * p + q] = (uint8_t)code;
+    }
+    lab[p] = (uint8_t)byte;
+  }
+}
