@@ -117,3 +117,70 @@ class HostDeltaCodec:
         for (pc, flags), c in zip(res, counts):
             B._raise_decode_flags(flags, pc, c)
         return self.out_h
+
+    def roundtrip(self, base_h: torch.Tensor, cur_h: torch.Tensor, lag: int = 4):
+        """Save + restore of one delta checkpoint through pinned host memory:
+        H2D of base and current once, encode, D2H of the record (mask +
+        payload), decode of that record onto the device copy of the base
+        (the previous checkpoint stays resident, as in chain replay,
+        store.py:441-454), D2H of the restored tensor.  Chunk i's decode is
+        issued `lag` chunks behind its encode on separate streams, so the
+        H2D copies of later chunks overlap the D2H copies of earlier ones;
+        the host learns each chunk's n_c from that chunk's event.
+        Returns (HostDeltaRecord, restored pinned tensor)."""
+        base_h, cur_h = base_h.view(torch.int16), cur_h.view(torch.int16)
+        main = torch.cuda.current_stream(self.dev)
+        if not hasattr(self, "dstreams"):
+            self.dstreams = [torch.cuda.Stream(self.dev) for _ in range(2)]
+            self.st_h = torch.empty((self.nchunks, 2), dtype=torch.int64, pin_memory=True)
+            self.dst = rt.new_status(self.dev, self.nchunks)
+        st_h, dst = self.st_h, self.dst
+        for s in self.streams + self.dstreams:
+            s.wait_stream(main)
+        ranges = list(self._ranges())
+        events, counts = [None] * self.nchunks, [0] * self.nchunks
+        offs = [0] * (self.nchunks + 1)
+
+        def encode(i, a, b):
+            s = self.streams[i % len(self.streams)]
+            with torch.cuda.stream(s):
+                self.b_d[a:b].copy_(base_h[a:b], non_blocking=True)
+                self.c_d[a:b].copy_(cur_h[a:b], non_blocking=True)
+                B.encode_delta_async(self.b_d[a:b], self.c_d[a:b], self.m_d[a // 8:(b + 7) // 8],
+                                     self.p_d[a:b], self.st[i])
+                st_h[i].copy_(self.st[i], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(s)
+                events[i] = ev
+
+        def finish(i, a, b):
+            events[i].synchronize()
+            c, flags = int(st_h[i, 0]), int(st_h[i, 1])
+            if flags:
+                raise B.DeltaError("internal: payload capacity exceeded")
+            counts[i] = c
+            offs[i + 1] = offs[i] + c
+            s = self.dstreams[i % len(self.dstreams)]
+            s.wait_event(events[i])
+            with torch.cuda.stream(s):
+                self.mask_h[a // 8:(b + 7) // 8].copy_(self.m_d[a // 8:(b + 7) // 8],
+                                                       non_blocking=True)
+                if c:
+                    self.payload_h[offs[i]:offs[i] + c].copy_(self.p_d[a:a + c],
+                                                              non_blocking=True)
+                B.decode_delta_async(self.b_d[a:b], self.m_d[a // 8:(b + 7) // 8],
+                                     self.p_d[a:a + c], c, self.c_d[a:b], dst[i])
+                self.out_h[a:b].copy_(self.c_d[a:b], non_blocking=True)
+
+        for i, a, b in ranges:
+            encode(i, a, b)
+            if i >= lag:
+                finish(*ranges[i - lag])
+        for i, a, b in ranges[max(0, self.nchunks - lag):]:
+            finish(i, a, b)
+        for s in self.streams + self.dstreams:
+            main.wait_stream(s)
+        for (pc, flags), c in zip(rt.read_status(dst), counts):
+            B._raise_decode_flags(flags, pc, c)
+        rec = HostDeltaRecord(self.mask_h, self.payload_h[:offs[-1]], self.n, offs[-1], counts)
+        return rec, self.out_h

@@ -230,3 +230,30 @@ def test_large_roundtrip_properties(dev, p):
     pos = torch.sort(idx).values
     assert torch.equal(d.payload, cur[pos])
     assert B.delta_size_bytes(n, k) == n // 8 + 2 * k + B.DELTA_FIXED_OVERHEAD
+
+
+def test_hostpath_roundtrip_matches_oracle(dev):
+    """hostpath.HostDeltaCodec.roundtrip (the bench's e2e path): the record
+    that lands in pinned host memory equals the oracle's, and the restored
+    tensor equals the current one (chunked, pipelined, odd tail)."""
+    import torch
+    from paper_2511_12376_b200 import hostpath
+    rng = np.random.default_rng(77)
+    n = 3 * (1 << 16) + 12345
+    base = rng.integers(0, 1 << 16, n, dtype=np.uint16)
+    cur = base.copy()
+    idx = rng.choice(n, n // 50, replace=False)
+    cur[idx] ^= rng.integers(1, 1 << 16, idx.size, dtype=np.uint16)
+    bh = torch.from_numpy(base.view(np.int16)).pin_memory()
+    ch = torch.from_numpy(cur.view(np.int16)).pin_memory()
+    codec = hostpath.HostDeltaCodec(dev, n, chunk=1 << 16)
+    for _ in range(2):
+        rec, out = codec.roundtrip(bh, ch)
+        mask, payload, n_c = O.delta_encode(base, cur)
+        assert rec.n_c == n_c
+        assert np.array_equal(rec.mask.numpy(), mask)
+        assert np.array_equal(rec.payload.numpy().view(np.uint16), payload)
+        assert np.array_equal(out.numpy().view(np.uint16), cur)
+    rec2 = codec.encode(bh, ch)
+    assert np.array_equal(rec2.mask.numpy(), mask)
+    assert np.array_equal(codec.decode(bh, rec2).numpy().view(np.uint16), cur)
