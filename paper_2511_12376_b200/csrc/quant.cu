@@ -443,33 +443,38 @@ __global__ void __launch_bounds__(kQThreads)
                       int* __restrict__ tile_mm, const uint32_t* __restrict__ need = nullptr) {
   __shared__ LabelLut L;
   __shared__ int wmin[kQThreads / 32][16], wmax[kQThreads / 32][16];
-  if (need) {  // only the units the threshold-window pass left undecided
-    const uint64_t full_tiles = (uint64_t)(P.nunits - 1) * P.T_full;
-    const uint32_t uu = blockIdx.x < full_tiles ? (uint32_t)(blockIdx.x / P.T_full) : P.nunits - 1;
-    if (!need[uu]) return;
-  }
-  const TileRef r = locate(P, blockIdx.x);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid < 16) L.bnd[tid] = fthr[r.u * 16 + tid];
-  if (lane < 16) {
-    wmin[warp][lane] = 0x7fffffff;
-    wmax[warp][lane] = (int)0x80000000;
-  }
-  __syncthreads();
-  lut_build_cta(L, (int)P.m);
-  const float* src = x + r.ustart + r.off;
-  const uint32_t size = (uint32_t)r.size;
-  if (L.ok) minmax_loop<true>(L, src, size, wmin[warp], wmax[warp]);
-  else minmax_loop<false>(L, src, size, wmin[warp], wmax[warp]);
-  __syncthreads();
-  if (tid < 16) {
-    int a = 0x7fffffff, b = (int)0x80000000;
-    for (int w = 0; w < kQThreads / 32; ++w) {
-      a = min(a, wmin[w][tid]);
-      b = max(b, wmax[w][tid]);
+  const uint64_t full_tiles = (uint64_t)(P.nunits - 1) * P.T_full;
+  // grid-stride over tiles: with `need`, only the units the threshold-window
+  // pass left undecided are visited (a small grid skips the rest quickly)
+  for (uint64_t tile = blockIdx.x; tile < P.total_tiles; tile += gridDim.x) {
+    if (need) {
+      const uint32_t uu = tile < full_tiles ? (uint32_t)(tile / P.T_full) : P.nunits - 1;
+      if (!need[uu]) continue;
     }
-    tile_mm[blockIdx.x * 32 + tid] = a;
-    tile_mm[blockIdx.x * 32 + 16 + tid] = b;
+    const TileRef r = locate(P, tile);
+    __syncthreads();  // the previous tile's reads of L / wmin / wmax are done
+    if (tid < 16) L.bnd[tid] = fthr[r.u * 16 + tid];
+    if (lane < 16) {
+      wmin[warp][lane] = 0x7fffffff;
+      wmax[warp][lane] = (int)0x80000000;
+    }
+    __syncthreads();
+    lut_build_cta(L, (int)P.m);
+    const float* src = x + r.ustart + r.off;
+    const uint32_t size = (uint32_t)r.size;
+    if (L.ok) minmax_loop<true>(L, src, size, wmin[warp], wmax[warp]);
+    else minmax_loop<false>(L, src, size, wmin[warp], wmax[warp]);
+    __syncthreads();
+    if (tid < 16) {
+      int a = 0x7fffffff, b = (int)0x80000000;
+      for (int w = 0; w < kQThreads / 32; ++w) {
+        a = min(a, wmin[w][tid]);
+        b = max(b, wmax[w][tid]);
+      }
+      tile_mm[tile * 32 + tid] = a;
+      tile_mm[tile * 32 + 16 + tid] = b;
+    }
   }
 }
 
@@ -1496,7 +1501,8 @@ int run_window(const float* x, const QPlan& P, bsnp_cluster_table* tables, uint8
   fit_decide_kernel<<<P.nunits, 32, 0, s>>>(P, w.ug, tables, w.need);
   if ((rc = launch_status("fit_decide_kernel"))) return rc;
   // exact per-element min/max, only for the units the window left undecided
-  fit_minmax_kernel<<<tiles, kQThreads, 0, s>>>(x, P, w.fthr, w.tile_mm, w.need);
+  fit_minmax_kernel<<<std::min(tiles, 4096u), kQThreads, 0, s>>>(x, P, w.fthr, w.tile_mm,
+                                                                  w.need);
   if ((rc = launch_status("fit_minmax_kernel"))) return rc;
   fit_finalize_kernel<<<P.nunits, kQThreads, 0, s>>>(P, w.tile_mm, tables, w.need);
   if ((rc = launch_status("fit_finalize_kernel"))) return rc;

@@ -27,6 +27,12 @@
 // delta = 160 sd / n: for dense data pred/succ are ~sd/(n pdf) away, so a
 // missing side (probability ~e^-19 per threshold) only costs the exact round.
 constexpr uint32_t kWDeltaNum = 160;
+constexpr int kWBins = 4096;            // label LUT bins over mu +- 2 sd
+constexpr uint32_t kLutN = 0x40u;       // LUT bit: the bin meets some [F_k - delta, F_k + delta]
+
+__device__ __forceinline__ uint32_t w_bin(float v, float gi, float c0) {
+  return min(__float2uint_rd(__fmaf_rn(v, gi, c0)), (uint32_t)kWBins - 1);
+}
 
 struct UGrid {
   float c0, gi, delta;
@@ -37,7 +43,7 @@ struct UGrid {
   float B32[16];          // quantize boundaries RN_f32(B64), +inf padded
   uint32_t lo[16];        // max ukey of candidates <= F_k; 0 = none
   uint32_t hi_c[16];      // ~(min ukey of candidates > F_k); 0 = none
-  uint8_t lut[kRBins];
+  uint8_t lut[kWBins];
 };
 constexpr size_t kUGridBytes = sizeof(UGrid);
 static_assert(sizeof(UGrid) % 16 == 0, "UGrid alignment");
@@ -45,8 +51,8 @@ static_assert(sizeof(UGrid) % 16 == 0, "UGrid alignment");
 __global__ void __launch_bounds__(kQThreads)
     fit_grid_kernel(QPlan P, const double* __restrict__ mu, const double* __restrict__ sdv,
                     const bsnp_cluster_table* __restrict__ tables, UGrid* __restrict__ ug) {
-  __shared__ int binB[16];
-  __shared__ float s_gi, s_c0;
+  __shared__ int binB[16], nlo[16], nhi[16];
+  __shared__ float s_gi, s_c0, s_delta;
   __shared__ uint32_t s_mode;
   const uint32_t u = blockIdx.x;
   const int tid = threadIdx.x, m = (int)P.m;
@@ -58,7 +64,7 @@ __global__ void __launch_bounds__(kQThreads)
   if (tid == 0) {
     const float r0 = __double2float_rn(__dsub_rn(m0, __dmul_rn(2.0, sd)));
     const float wd = __double2float_rn(__dmul_rn(4.0, sd));
-    const float gi = __fdiv_rn((float)kRBins, wd);
+    const float gi = __fdiv_rn((float)kWBins, wd);
     const float c0 = -__fmul_rn(r0, gi);
     const bool ok = isfinite(r0) && isfinite(gi) && gi > 0.0f && isfinite(c0) &&
                     isfinite(m0) && isfinite(sd);
@@ -67,7 +73,8 @@ __global__ void __launch_bounds__(kQThreads)
     s_mode = ok ? 0u : 3u;
     G.gi = gi;
     G.c0 = c0;
-    G.delta = __double2float_ru(__ddiv_rn(__dmul_rn((double)kWDeltaNum, sd), (double)len));
+    s_delta = __double2float_ru(__ddiv_rn(__dmul_rn((double)kWDeltaNum, sd), (double)len));
+    G.delta = s_delta;
     G.gmax = 0;
     G.gmin_c = 0;
   }
@@ -83,7 +90,11 @@ __global__ void __launch_bounds__(kQThreads)
     G.B32[tid] = r;
     G.lo[tid] = 0;
     G.hi_c[tid] = 0;
-    binB[tid] = tid < m - 1 ? (int)r_bin(r, s_gi, s_c0) : 0x3fffffff;
+    binB[tid] = tid < m - 1 ? (int)w_bin(r, s_gi, s_c0) : 0x3fffffff;
+    // bins meeting the window around F_k (monotone bins: |v - F| < delta
+    // implies bin(F - delta) <= bin(v) <= bin(F + delta))
+    nlo[tid] = tid < m - 1 ? (int)w_bin(__fsub_rd(f, s_delta), s_gi, s_c0) : 0x3fffffff;
+    nhi[tid] = tid < m - 1 ? (int)w_bin(__fadd_ru(f, s_delta), s_gi, s_c0) : -1;
   }
   __syncthreads();
   if (tid == 0) {
@@ -93,21 +104,24 @@ __global__ void __launch_bounds__(kQThreads)
     s_mode = mode;
     G.mode = mode;
   }
-  // thread t: bins [4t, 4t + 4)
-  static_assert(kRBins == 4 * kQThreads, "4 LUT bins per thread");
-  const int b0 = 4 * tid;
+  __syncthreads();
+  // thread t: bins [16t, 16t + 16)
+  static_assert(kWBins == 16 * kQThreads, "16 LUT bins per thread");
+  const int b0 = 16 * tid;
   int cnt = 0;
   for (int k = 0; k < m - 1; ++k) cnt += binB[k] < b0;
-  uint32_t w = 0;
+  uint32_t w[4] = {0, 0, 0, 0};
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < 16; ++q) {
     const int bb = b0 + q;
     while (cnt < m - 1 && binB[cnt] < bb) ++cnt;
     uint32_t e = (uint32_t)cnt;
     if (cnt < m - 1 && binB[cnt] == bb) e |= kLutB;
-    w |= e << (8 * q);
+    for (int k = 0; k < m - 1; ++k)
+      if (nlo[k] <= bb && bb <= nhi[k]) e |= kLutN;
+    w[q >> 2] |= e << (8 * (q & 3));
   }
-  reinterpret_cast<uint32_t*>(G.lut)[tid] = w;
+  reinterpret_cast<uint4*>(G.lut)[tid] = make_uint4(w[0], w[1], w[2], w[3]);
 }
 
 // elementwise passes run over kDqChunk-element chunks of each unit (the
@@ -135,7 +149,7 @@ __device__ __forceinline__ ChunkRef chunk_of(const QPlan& P, uint64_t cidx) {
 }
 
 struct WSmem {
-  uint8_t lut[kRBins];
+  __align__(16) uint8_t lut[kWBins];
   float F[16], B32[16];
   float2 FF[16];  // (F[c-1], F[c]) around quantize cluster c
   uint32_t lo[16], hi_c[16];
@@ -146,7 +160,17 @@ struct WSmem {
 
 __device__ __forceinline__ uint32_t w_label(const WSmem& S, float v, bool cmp) {
   if (cmp) return count_below(S.B32, v);
-  const uint32_t le = S.lut[r_bin(v, S.gi, S.c0)];
+  const uint32_t le = S.lut[w_bin(v, S.gi, S.c0)];
+  const uint32_t L = le & 15u;
+  return L + ((le >> 7) & (v > S.B32[L] ? 1u : 0u));
+}
+
+// label + "maybe within delta of a fit threshold" from one LUT byte
+template <bool kCmp>
+__device__ __forceinline__ uint32_t w_label_n(const WSmem& S, float v, uint32_t& near) {
+  const uint32_t le = S.lut[w_bin(v, S.gi, S.c0)];
+  near |= le;
+  if (kCmp) return count_below(S.B32, v);
   const uint32_t L = le & 15u;
   return L + ((le >> 7) & (v > S.B32[L] ? 1u : 0u));
 }
@@ -174,25 +198,38 @@ __device__ __forceinline__ void w_label_loop(WSmem& S, const float* src, uint32_
   const int tid = threadIdx.x;
   const bool vec = ((((uintptr_t)src) & 15) | (((uintptr_t)lab) & 1)) == 0;
   const uint32_t nv = vec ? size / 4 : 0;
-#pragma unroll 4
-  for (uint32_t i = tid; i < nv; i += kQThreads) {
-    const float4 v4 = ld_stream_f4(src + 4 * i);
-    const float v[4] = {v4.x, v4.y, v4.z, v4.w};
-    uint32_t c[4];
-    bool nb = false;
+  constexpr int kB = 4;  // vectors per thread in flight
+  for (uint32_t i0 = tid; i0 < nv; i0 += kB * kQThreads) {
+    float4 v4[kB];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      c[q] = w_label(S, v[q], kCmp);
-      nb |= w_near(S, v[q], c[q]);
+    for (int b = 0; b < kB; ++b) {
+      const uint32_t i = i0 + b * kQThreads;
+      if (i < nv) v4[b] = ld_stream_f4(src + 4 * i);
     }
-    vmin = fmin3(vmin, fminf(v[0], v[1]), fminf(v[2], v[3]));
-    vmax = fmax3(vmax, fmaxf(v[0], v[1]), fmaxf(v[2], v[3]));
-    if (lab)
-      *reinterpret_cast<uint16_t*>(lab + 2 * i) =
-          (uint16_t)(c[0] | (c[1] << 4) | (c[2] << 8) | (c[3] << 12));
-    if (__builtin_expect(nb, 0)) {
-      for (int q = 0; q < 4; ++q)
-        if (w_near(S, v[q], c[q])) w_candidates(S, v[q], c[q], m);
+#pragma unroll
+    for (int b = 0; b < kB; ++b) {
+      const uint32_t i = i0 + b * kQThreads;
+      if (i >= nv) break;
+      const float v[4] = {v4[b].x, v4[b].y, v4[b].z, v4[b].w};
+      uint32_t le[4], c[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        le[q] = S.lut[w_bin(v[q], S.gi, S.c0)];
+        c[q] = kCmp ? count_below(S.B32, v[q]) : (le[q] & 15u);
+      }
+      vmin = fmin3(vmin, fminf(v[0], v[1]), fminf(v[2], v[3]));
+      vmax = fmax3(vmax, fmaxf(v[0], v[1]), fmaxf(v[2], v[3]));
+      if (__builtin_expect(((le[0] | le[1] | le[2] | le[3]) & (kLutB | kLutN)) != 0, 0)) {
+        // rare: a quantize boundary inside the bin, or a fit threshold near
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (!kCmp && (le[q] & kLutB)) c[q] += v[q] > S.B32[c[q]] ? 1u : 0u;
+          if ((le[q] & kLutN) && w_near(S, v[q], c[q])) w_candidates(S, v[q], c[q], m);
+        }
+      }
+      if (lab)
+        *reinterpret_cast<uint16_t*>(lab + 2 * i) =
+            (uint16_t)(c[0] | (c[1] << 4) | (c[2] << 8) | (c[3] << 12));
     }
   }
   // tail (and unaligned tiles): element pairs (one label byte each)
@@ -217,7 +254,7 @@ __global__ void __launch_bounds__(kQThreads)
   const ChunkRef r = chunk_of(P, blockIdx.x);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, m = (int)P.m;
   UGrid& G = ug[r.u];
-  reinterpret_cast<uint32_t*>(S.lut)[tid] = reinterpret_cast<const uint32_t*>(G.lut)[tid];
+  reinterpret_cast<uint4*>(S.lut)[tid] = reinterpret_cast<const uint4*>(G.lut)[tid];
   if (tid < 16) {
     const float f = G.F[tid];
     S.F[tid] = f;
@@ -295,15 +332,17 @@ __global__ void __launch_bounds__(32)
   tb.offsets[c] = offset;
 }
 
-// codes of one tile from x and its written labels (quantizer.py:174-182)
+// codes of one chunk from x and its written labels (quantizer.py:174-182).
+// Labels are only read here: a NaN element keeps the label of stage C (its
+// unit is non-finite and the host raises QuantizerError).
 __global__ void __launch_bounds__(kQThreads)
     quantize_codes_kernel(const float* __restrict__ x, QPlan P,
                           const bsnp_cluster_table* __restrict__ tables,
-                          uint8_t* __restrict__ labels, uint8_t* __restrict__ codes) {
+                          const uint8_t* __restrict__ labels, uint8_t* __restrict__ codes) {
   __shared__ float2 qp[16];
   __shared__ float qs[16];
   const ChunkRef r = chunk_of(P, blockIdx.x);
-  const int tid = threadIdx.x, m = (int)P.m;
+  const int tid = threadIdx.x;
   const bsnp_cluster_table& tb = tables[r.u];
   if (tid < 16) {
     const float S_ = tb.scales[tid];
@@ -318,60 +357,60 @@ __global__ void __launch_bounds__(kQThreads)
   __syncthreads();
   const float* src = x + r.ustart + r.c0;
   uint8_t* cdst = codes + r.ustart + r.c0;
-  uint8_t* lab = labels + (uint64_t)r.u * (P.block / 2) + r.c0 / 2;
+  const uint8_t* lab = labels + (uint64_t)r.u * (P.block / 2) + r.c0 / 2;
   const uint32_t size = (uint32_t)r.len;
   const bool vec = ((((uintptr_t)src) & 15) | (((uintptr_t)cdst) & 3) | (((uintptr_t)lab) & 1)) == 0;
   const uint32_t nv = vec ? size / 4 : 0;
-#pragma unroll 4
-  for (uint32_t i = tid; i < nv; i += kQThreads) {
-    const float4 v4 = ld_stream_f4(src + 4 * i);
-    const float v[4] = {v4.x, v4.y, v4.z, v4.w};
-    const uint32_t lw = *reinterpret_cast<const uint16_t*>(lab + 2 * i);
-    uint32_t code[4];
-    bool amb = false;
+  constexpr int kB = 4;  // vectors per thread in flight
+  for (uint32_t i0 = tid; i0 < nv; i0 += kB * kQThreads) {
+    float4 v4[kB];
+    uint32_t lw[kB];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float2 bp = qp[(lw >> (4 * q)) & 15u];
-      // within 6.2e-5 of 255(v-b)/S - 0.5: exact unless flagged ambiguous;
-      // the saturation is the reference's clip (labels vs RN boundaries can
-      // put v just outside the [b, b+S] of the fit's RD thresholds)
-      const float tt = __fsub_rn(__fmul_rn(__fsub_rn(v[q], bp.x), bp.y), 0.5f);
-      amb |= !(fabsf(__fsub_rn(tt, rintf(tt))) > 0.000244140625f);  // also NaN
-      code[q] = ceil_u8(tt);
+    for (int b = 0; b < kB; ++b) {
+      const uint32_t i = i0 + b * kQThreads;
+      if (i < nv) {
+        v4[b] = ld_stream_f4(src + 4 * i);
+        lw[b] = __ldg(reinterpret_cast<const uint16_t*>(lab) + i);
+      }
     }
-    if (__builtin_expect(amb, 0)) {
-      uint32_t lw2 = lw;
+#pragma unroll
+    for (int b = 0; b < kB; ++b) {
+      const uint32_t i = i0 + b * kQThreads;
+      if (i >= nv) break;
+      const float v[4] = {v4[b].x, v4[b].y, v4[b].z, v4[b].w};
+      uint32_t code[4];
+      bool amb = false;
+#pragma unroll
       for (int q = 0; q < 4; ++q) {
-        uint32_t c = (lw >> (4 * q)) & 15u;
-        bool a1 = false;
-        code_estimate(v[q], qp[c].x, qp[c].y, a1);
-        if (a1) {
-          if (isnan(v[q])) {  // numpy sorts NaN after every boundary
-            c = (uint32_t)(m - 1);
-            lw2 = (lw2 & ~(15u << (4 * q))) | (c << (4 * q));
-          }
-          code[q] = exact_code(v[q], qp[c].x, qs[c]);
+        const float2 bp = qp[(lw[b] >> (4 * q)) & 15u];
+        // within 6.2e-5 of 255(v-b)/S - 0.5: exact unless flagged ambiguous;
+        // the saturation is the reference's clip (labels vs RN boundaries can
+        // put v just outside the [b, b+S] of the fit's RD thresholds)
+        const float tt = __fsub_rn(__fmul_rn(__fsub_rn(v[q], bp.x), bp.y), 0.5f);
+        amb |= !(fabsf(__fsub_rn(tt, rintf(tt))) > 0.000244140625f);  // also NaN
+        code[q] = ceil_u8(tt);
+      }
+      if (__builtin_expect(amb, 0)) {
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t c = (lw[b] >> (4 * q)) & 15u;
+          bool a1 = false;
+          code_estimate(v[q], qp[c].x, qp[c].y, a1);
+          if (a1) code[q] = exact_code(v[q], qp[c].x, qs[c]);
         }
       }
-      if (lw2 != lw) *reinterpret_cast<uint16_t*>(lab + 2 * i) = (uint16_t)lw2;
+      *reinterpret_cast<uint32_t*>(cdst + 4 * i) =
+          code[0] | (code[1] << 8) | (code[2] << 16) | (code[3] << 24);
     }
-    *reinterpret_cast<uint32_t*>(cdst + 4 * i) =
-        code[0] | (code[1] << 8) | (code[2] << 16) | (code[3] << 24);
   }
   for (uint32_t p = 2 * nv + tid; 2 * p < size; p += kQThreads) {
-    uint32_t byte = lab[p];
+    const uint32_t byte = lab[p];
     for (uint32_t q = 0; q < 2 && 2 * p + q < size; ++q) {
       const float v = src[2 * p + q];
-      uint32_t c = (byte >> (4 * q)) & 15u;
-      if (isnan(v)) {
-        c = (uint32_t)(m - 1);
-        byte = (byte & ~(15u << (4 * q))) | (c << (4 * q));
-      }
+      const uint32_t c = (byte >> (4 * q)) & 15u;
       bool a1 = false;
-      uint32_t code = min(code_estimate(v, qp[c].x, qp[c].y, a1), 255u);
+      uint32_t code = code_estimate(v, qp[c].x, qp[c].y, a1);
       if (a1) code = exact_code(v, qp[c].x, qs[c]);
       cdst[2 * p + q] = (uint8_t)code;
     }
-    lab[p] = (uint8_t)byte;
   }
 }
