@@ -1,0 +1,147 @@
+#!/usr/bin/env python
+"""Whole-checkpoint codec benchmark (BASELINE configs[0] "C0" and [3] "C3").
+
+A checkpoint pair (base at iteration 0, delta at iteration 1) of a
+GPT-2-small (C0) or Llama-2-7B (C3) shaped model is generated on the GPU
+(SURVEY §8(d) recipe: fp32 master w0 ~ N(0, 0.02), w1 = w0 - 1e-5 u, saved
+weights bf16; Adam m ~ N(0, 1e-3), v = N(0, 1e-3)^2, quantized per tensor
+with m = 16 clusters as store.encode_checkpoint does).  Timed with CUDA
+events, inputs resident in HBM, outputs landing in pinned host memory:
+
+  save_base   encode_checkpoint(kind=base)   RAW model + QUANT optimizer
+  save_delta  encode_checkpoint(kind=delta)  DELTA model vs the resident
+                                             previous states + QUANT
+  load        decode_chain([base, delta])    RAW + in-place delta replay +
+                                             dequantize (host blobs in)
+
+GB/s = raw checkpoint bytes / time.  --verify re-encodes C0 with the CPU
+oracle (numpy restatement of the reference) and compares the blobs.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def shapes(config: str):
+    if config == "C0":
+        d, ffn, vocab, ctx, layers = 768, 3072, 50257, 1024, 12
+        out = [("wte", (vocab, d)), ("wpe", (ctx, d))]
+        for i in range(layers):
+            p = f"h.{i}."
+            out += [(p + "ln_1.w", (d,)), (p + "ln_1.b", (d,)),
+                    (p + "attn.c_attn.w", (d, 3 * d)), (p + "attn.c_attn.b", (3 * d,)),
+                    (p + "attn.c_proj.w", (d, d)), (p + "attn.c_proj.b", (d,)),
+                    (p + "ln_2.w", (d,)), (p + "ln_2.b", (d,)),
+                    (p + "mlp.c_fc.w", (d, ffn)), (p + "mlp.c_fc.b", (ffn,)),
+                    (p + "mlp.c_proj.w", (ffn, d)), (p + "mlp.c_proj.b", (d,))]
+        return out + [("ln_f.w", (d,)), ("ln_f.b", (d,))]
+    if config == "C3":
+        d, ffn, vocab, layers = 4096, 11008, 32000, 32
+        out = [("embed", (vocab, d)), ("lm_head", (vocab, d)), ("norm", (d,))]
+        for i in range(layers):
+            p = f"layers.{i}."
+            out += [(p + n, (d, d)) for n in ("q", "k", "v", "o")]
+            out += [(p + "gate", (ffn, d)), (p + "up", (ffn, d)), (p + "down", (d, ffn)),
+                    (p + "in_norm", (d,)), (p + "post_norm", (d,))]
+        return out
+    raise ValueError(config)
+
+
+def generate(config: str, dev, seed: int = 0):
+    import torch
+    from paper_2511_12376_b200.store import DeviceTensor
+    from paper_2511_12376_b200.tensors import Checkpoint
+    g = torch.Generator(device=dev).manual_seed(seed)
+    base, cur, opt = [], [], []
+    for name, shp in shapes(config):
+        w0 = torch.randn(shp, device=dev, generator=g) * 0.02
+        w1 = w0 - 1e-5 * torch.randn(shp, device=dev, generator=g)
+        base.append(DeviceTensor.wrap(name, w0.to(torch.bfloat16)))
+        cur.append(DeviceTensor.wrap(name, w1.to(torch.bfloat16)))
+        del w0, w1
+        opt.append(DeviceTensor.wrap("adam.m." + name,
+                                     torch.randn(shp, device=dev, generator=g) * 1e-3))
+        opt.append(DeviceTensor.wrap("adam.v." + name,
+                                     (torch.randn(shp, device=dev, generator=g) * 1e-3) ** 2))
+    return (Checkpoint(iteration=0, model_states=base, optimizer_states=opt),
+            Checkpoint(iteration=1, model_states=cur, optimizer_states=opt))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="C0", choices=["C0", "C3"])
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--verify", action="store_true")
+    args = ap.parse_args()
+    import torch
+    from paper_2511_12376_b200 import store as S
+    dev = torch.device("cuda:0")
+    c0, c1 = generate(args.config, dev)
+    raw = sum(t.nbytes for t in c1.model_states + c1.optimizer_states)
+    enc = S.CheckpointEncoder(dev, clusters=16)
+
+    def timed(fn):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        out = fn()
+        torch.cuda.synchronize()
+        return out, time.perf_counter() - t
+
+    res = {}
+    for _ in range(args.reps):
+        (m0, b0), tb = timed(lambda: enc.encode(c0, None, S.KIND_BASE))
+        (m1, b1), td = timed(lambda: enc.encode(c1, None, S.KIND_DELTA))
+        blob0, blob1 = b0.numpy().tobytes(), b1.numpy().tobytes()
+        chain = [(m0, blob0), (m1, blob1)]
+        out, tl = timed(lambda: S.decode_chain(chain, to_host=False))
+        for k, v in (("save_base_s", tb), ("save_delta_s", td), ("load_s", tl)):
+            res[k] = min(res.get(k, 1e9), v)
+    # correctness of the round trip on the device
+    for a, b in zip(out.model_states, c1.model_states):
+        assert torch.equal(a.data.view(torch.int16), b.flat())
+    codecs = {}
+    for e in m1.tensors:
+        codecs[e.codec] = codecs.get(e.codec, 0) + 1
+    mb = sum(t.nbytes for t in c1.model_states)
+    ob = sum(t.nbytes for t in c1.optimizer_states)
+    mlen = sum(e.length for e in m1.tensors if e.group == "model")
+    olen = sum(e.length for e in m1.tensors if e.group == "optimizer")
+    line = {
+        "config": args.config, "tensors": len(m1.tensors), "raw_bytes": raw,
+        "codecs_delta_checkpoint": codecs,
+        "ratio_weights": round(mb / mlen, 4), "ratio_optimizer": round(ob / olen, 4),
+        "ratio_total": round(raw / len(blob1), 4),
+        "save_base_gbs": round(raw / res["save_base_s"] / 1e9, 2),
+        "save_delta_gbs": round(raw / res["save_delta_s"] / 1e9, 2),
+        "load_gbs": round(raw / res["load_s"] / 1e9, 2),
+        **{k: round(v, 4) for k, v in res.items()},
+        "note": "device-resident inputs; outputs in pinned host memory (D2H included); "
+                "load starts from host blobs (H2D included)",
+    }
+    if args.verify and args.config == "C0":
+        import numpy as np
+        from oracle import bitsnap_oracle as O
+
+        def conv(ts, code):
+            return [(t.name, t.shape, code, t.flat().cpu().numpy().view(
+                np.uint16 if code == 0 else np.float32)) for t in ts]
+        t = time.perf_counter()
+        entries, want = O.encode_checkpoint(conv(c1.model_states, 0),
+                                            conv(c1.optimizer_states, 1),
+                                            conv(c0.model_states, 0), "delta", 16)
+        line["oracle_delta_encode_s"] = round(time.perf_counter() - t, 2)
+        line["oracle_blob_identical"] = want == blob1
+        line["oracle_manifest_identical"] = entries == [vars(e) for e in m1.tensors]
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()
