@@ -446,6 +446,12 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # BSNP_DIST_BACKEND=gloo (test only): exercise the multi-rank code path
+    # with several ranks sharing fewer GPUs; the driver's runs use NCCL
+    backend = os.environ.get("BSNP_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        import torch
+        local_rank %= max(1, torch.cuda.device_count())
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -453,7 +459,10 @@ def main():
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     try:
         run_b200(args, rank, world, local_rank)
     finally:
