@@ -130,9 +130,6 @@ __device__ __forceinline__ uint32_t lut_label(const LabelLut& L, float v) {
   return (e & 0xffu) + (L.bnd[e >> 8] < v ? 1u : 0u);
 }
 
-__device__ __forceinline__ uint32_t label_of(const LabelLut& L, float v) {
-  return L.ok ? lut_label(L, v) : count_below(L.bnd, v);
-}
 
 // CTA-wide build of a label LUT (threads 0..63 build, all threads vote).
 // L.bnd[] (+inf padded) must be visible to every thread before the call.
@@ -724,561 +721,6 @@ __global__ void __launch_bounds__(kQThreads)
   }
 }
 
-// ===========================================================================
-// Fused per-block encoder (B200-native path for power-of-two blocks).
-//
-// One thread-block cluster of kC CTAs owns one block (unit) at a time; CTA
-// rank r owns the contiguous slice [r*block/kC, (r+1)*block/kC), i.e. a
-// perfect sub-tree of numpy's pairwise tree made of T tiles of 8192 elements.
-// The four passes of build_clusters + quantize (sum, centred sum of squares,
-// per-cluster min/max, quantize) stream the slice's tiles through a ring of
-// kSlots shared-memory slots filled by cp.async.bulk (one 512 B copy per
-// 128-float chunk, padded layout); each pass first consumes the tiles still
-// resident from the previous pass, so only T - kSlots tiles per pass come back
-// from L2.  A producer warp runs the ring ahead of the 8 consumer warps
-// (mbarriers full/empty); the three cross-CTA reductions per block go through
-// DSMEM (remote mbarrier arrive + ld.shared::cluster), never through HBM.
-// ===========================================================================
-constexpr int kBWarps = 16;                   // consumer warps
-constexpr int kBCons = kBWarps * 32;          // consumer threads
-constexpr int kBThreads = kBCons + 32;        // + 1 producer warp
-constexpr int kSlots = 6;
-constexpr uint32_t kTileF = 8192;
-constexpr uint32_t kQuarter = kTileF / 4;                       // 2048 floats = 8 KiB
-constexpr uint32_t kQStride = kQuarter + 8;                     // +8 floats per quarter
-constexpr uint32_t kSlotFloats = 4 * kQStride;                  // 8224
-constexpr uint32_t kSlotBytes = kSlotFloats * 4;
-constexpr int kMaxT = 32;  // tiles per CTA slice (leaf sums of all tiles stay in smem)
-
-#ifdef BSNP_WATCHDOG
-__device__ unsigned long long g_wd_log[64][4];
-__device__ unsigned int g_wd_n;
-__device__ unsigned int g_wd_prog[1024][10];  // per CTA: producer k, consumer warp k
-__device__ __forceinline__ void wd_prog(int slot, uint32_t k) {
-  if ((threadIdx.x & 31) == 0) *(volatile unsigned*)&g_wd_prog[blockIdx.x][slot] = k;
-}
-__device__ __forceinline__ void wd_record(uint32_t site, uint32_t a, uint32_t b, uint32_t c) {
-  if (threadIdx.x & 31) return;
-  const unsigned i = atomicAdd(&g_wd_n, 1u);
-  if (i < 64) {
-    uint32_t rank;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
-    g_wd_log[i][0] = ((unsigned long long)site << 32) | (blockIdx.x << 8) | (threadIdx.x >> 5);
-    g_wd_log[i][1] = a | ((unsigned long long)(*(volatile unsigned*)&g_wd_prog[blockIdx.x][9]) << 32);
-    g_wd_log[i][2] = b;
-    g_wd_log[i][3] = ((unsigned long long)rank << 32) | c;
-  }
-}
-// bounded try_wait: returns false on timeout
-__device__ __forceinline__ bool wd_wait(uint64_t* bar, uint32_t parity, bool cluster_scope) {
-  for (uint32_t it = 0; it < (1u << 22); ++it) {
-    uint32_t ok;
-    if (cluster_scope)
-      asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n}"
-                   : "=r"(ok) : "r"(smem_addr(bar)), "r"(parity) : "memory");
-    else
-      asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n}"
-                   : "=r"(ok) : "r"(smem_addr(bar)), "r"(parity) : "memory");
-    if (ok) return true;
-  }
-  return false;
-}
-#define WD_WAIT(bar, par, site, a, b, c) \
-  do { if (!wd_wait(bar, par, false)) wd_record(site, a, b, c); } while (0)
-#define WD_WAITC(bar, par, site, a, b, c) \
-  do { if (!wd_wait(bar, par, true)) wd_record(site, a, b, c); } while (0)
-#define WD_PROG(slot, k) wd_prog(slot, k)
-__device__ unsigned long long g_tm[8];  // cycles: wait_full, p0, p1, p2, p3, sync, exchange, total
-#define TM_DECL unsigned long long _tm0 = clock64(), _tm1;
-#define TM_MARK(cat) do { _tm1 = clock64(); if (threadIdx.x == 0) atomicAdd(&g_tm[cat], _tm1 - _tm0); _tm0 = _tm1; } while (0)
-#else
-#define WD_PROG(slot, k)
-#define TM_DECL
-#define TM_MARK(cat)
-#define WD_WAIT(bar, par, site, a, b, c) mbar_wait(bar, par)
-#define WD_WAITC(bar, par, site, a, b, c) mbar_wait_acq_cluster(bar, par)
-#endif
-
-__device__ __forceinline__ uint32_t cluster_ctarank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ uint32_t cluster_idx() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ uint32_t cluster_count() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ uint32_t dsmem_addr(const void* local, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr(local)), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAITC_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAITC_%=;\n}" ::"r"(smem_addr(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ double ld_dsmem_f64(uint32_t a) {
-  double v;
-  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
-  return v;
-}
-__device__ __forceinline__ int ld_dsmem_s32(uint32_t a) {
-  int v;
-  asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
-  return v;
-}
-__device__ __forceinline__ void cluster_barrier() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
-                   : "memory");
-}
-__device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t* p) {
-  return *(const volatile uint32_t*)p;
-}
-__device__ __forceinline__ void st_volatile_u32(uint32_t* p, uint32_t v) {
-  *(volatile uint32_t*)p = v;
-}
-__device__ __forceinline__ void consumers_sync() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kBCons) : "memory");
-}
-// AND-vote across the consumer threads (named barrier 1)
-__device__ __forceinline__ bool consumers_and(bool v) {
-  uint32_t r;
-  asm volatile(
-      "{\n\t.reg .pred p, q;\n\tsetp.ne.u32 p, %1, 0;\n\t"
-      "bar.red.and.pred q, 1, %2, p;\n\tselp.u32 %0, 1, 0, q;\n}"
-      : "=r"(r)
-      : "r"((uint32_t)v), "n"(kBCons)
-      : "memory");
-  return r != 0;
-}
-
-// builder threads (b = 0..63) build one table (bnd[] already set); every
-// consumer thread calls it for the vote
-__device__ void lut_build(LabelLut& L, int m, int b, bool builder) {
-  const float g0 = L.bnd[0], g1 = L.bnd[m > 2 ? m - 2 : 0];
-  const float ginv = __fdiv_rn(64.0f, __fsub_rn(g1, g0));
-  const bool usable = m > 2 && g1 > g0 && isfinite(ginv) && ginv > 0.0f;
-  uint32_t base = 0, kin = 15, cnt = 0;
-  if (builder) {
-    for (int k = 0; k < m - 1; ++k) {
-      const int bk = lut_bin(L.bnd[k], g0, ginv);
-      if (bk < b) ++base;
-      else if (bk == b) {
-        kin = (uint32_t)k;
-        ++cnt;
-      }
-    }
-    L.ent[b] = base | (kin << 8);
-  }
-  const bool ok = consumers_and(usable && cnt <= 1);
-  if (builder && b == 0) {
-    L.g0 = g0;
-    L.ginv = ginv;
-    L.ok = ok ? 1u : 0u;
-  }
-}
-
-
-// slot offset of tile element e: quarters are 8 floats apart in bank space
-__device__ __forceinline__ uint32_t qpad(uint32_t e) { return e + ((e / kQuarter) << 3); }
-
-constexpr int kSched = 16;  // producer -> consumers schedule ring (>= kSlots + 1)
-
-struct BlockSmem {
-  uint64_t full[kSlots], xbar[2];
-  double leafsum[kMaxT][64];     // per tile; reduced to tile sums at the end of a pass
-  uint32_t wconsumed[kBWarps];  // items consumed per consumer warp (monotonic)
-  uint32_t published;  // items whose schedule entry is written (monotonic)
-  uint32_t sched[kSched];  // item k: tile | load << 8
-  double tsum[kMaxT];
-  double xval[2];
-  int xmm[2][32];
-  int smin[16], smax[16];
-  int wmin[kBWarps][16], wmax[kBWarps][16];  // per-warp extrema (no cross-warp contention)
-  double mu, sd;
-  LabelLut lf, lb;  // fit thresholds RD(B64), quantize boundaries RN(B64)
-  float2 qp[16];    // {offset, 255/S}
-  float qs[16];     // S
-  uint32_t qlast;
-};
-
-// slowest consumer warp's progress (the producer's slot-release signal)
-__device__ __forceinline__ uint32_t min_consumed(const BlockSmem& B) {
-  uint32_t m = 0xffffffffu;
-#pragma unroll
-  for (int w = 0; w < kBWarps; ++w) m = min(m, ld_volatile_u32(&B.wconsumed[w]));
-  return m;
-}
-
-// slot-ring schedule shared by producer and consumers (identical simulation)
-struct Ring {
-  uint32_t sunit[kSlots];
-  int stile[kSlots];
-  __device__ void init() {
-    for (int s = 0; s < kSlots; ++s) {
-      sunit[s] = 0xffffffffu;
-      stile[s] = -1;
-    }
-  }
-};
-
-// perfect-tree sum of n (power of two) values, left to right
-__device__ __forceinline__ double perfect_sum(const double* v, int n) {
-  double stk[8];
-  int lvl[8];
-  int top = 0;
-  for (int i = 0; i < n; ++i) {
-    double a = v[i];
-    int l = 0;
-    while (top > 0 && lvl[top - 1] == l) {
-      a = __dadd_rn(stk[top - 1], a);
-      --top;
-      ++l;
-    }
-    stk[top] = a;
-    lvl[top] = l;
-    ++top;
-  }
-  return stk[0];
-}
-
-// Pairwise sums of the 64 leaves (128 elements each) of one 8192-element
-// tile.  8 lanes per leaf, lane j owns numpy's accumulator r[j] = a[j] +
-// a[8+j] + ... (sequential); warp w takes leaves w, w+16, w+32, w+48, which
-// sit in different quarters of the slot and so hit distinct banks.
-template <bool kVar>
-__device__ __forceinline__ void tile_leaf_sums(const float* s, double mu, double* leafsum) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = warp + 16 * (lane >> 3), j = lane & 7;
-  const float* leaf = s + qpad(g * 128) + j;
-  float a[16];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) a[i] = leaf[8 * i];
-  double r = widen<kVar>(a[0], mu);
-#pragma unroll
-  for (int i = 1; i < 16; ++i) r = __dadd_rn(r, widen<kVar>(a[i], mu));
-  r = __dadd_rn(r, __shfl_xor_sync(kFull, r, 1));  // r0+r1 | r2+r3 | ...
-  r = __dadd_rn(r, __shfl_xor_sync(kFull, r, 2));  // (r0+r1)+(r2+r3) | (r4+r5)+(r6+r7)
-  r = __dadd_rn(r, __shfl_xor_sync(kFull, r, 4));  // leaf sum
-  if (j == 0) leafsum[g] = r;
-}
-
-// perfect tree over the 64 leaf sums (one warp): tile sum on every lane
-__device__ __forceinline__ double tile_sum_from_leaves(const double* leafsum, int lane) {
-  double v = __dadd_rn(leafsum[2 * lane], leafsum[2 * lane + 1]);
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) v = __dadd_rn(v, __shfl_xor_sync(kFull, v, d));
-  return v;
-}
-
-template <int kC>
-__global__ void __launch_bounds__(kBThreads, 1)
-    quant_block_kernel(const float* __restrict__ x, uint32_t nunits, uint64_t block, int m,
-                       bsnp_cluster_table* __restrict__ tables, uint8_t* __restrict__ labels,
-                       uint8_t* __restrict__ codes, int do_quant) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  float* slots = reinterpret_cast<float*>(smem);
-  BlockSmem& B = *reinterpret_cast<BlockSmem*>(smem + kSlots * kSlotBytes);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t rank = cluster_ctarank(), cid = cluster_idx(), ncl = cluster_count();
-  const uint64_t slice = block / kC;
-  const int T = (int)(slice / kTileF);
-  const int npass = do_quant ? 4 : 3;
-
-  if (tid == 0) {
-    for (int s = 0; s < kSlots; ++s) mbar_init(&B.full[s], 1);
-    for (int w = 0; w < kBWarps; ++w) B.wconsumed[w] = 0;
-    B.published = 0;
-    mbar_init(&B.xbar[0], kC);
-    mbar_init(&B.xbar[1], kC);
-    fence_mbar_init();
-  }
-  cluster_barrier();  // every CTA's barriers exist before any remote arrive
-
-  Ring ring;
-  ring.init();
-  if (warp == kBWarps) {
-    // ------------------------------------------------------------ producer
-    const uint64_t pol_last = policy_evict_first(), pol_keep = policy_evict_normal();
-    uint32_t k = 0;
-    for (uint32_t u = cid; u < nunits; u += ncl) {
-      const float* src_slice = x + (uint64_t)u * block + rank * slice;
-      for (int p = 0; p < npass; ++p) {
-        uint64_t res = 0, done = 0;
-        for (int s = 0; s < kSlots; ++s)
-          if (ring.sunit[s] == u) res |= 1ull << ring.stile[s];
-        int nxt = 0;
-        for (int i = 0; i < T; ++i, ++k) {
-          const int s = k % kSlots;
-          int t;
-          bool load;
-          if (ring.sunit[s] == u && !((done >> ring.stile[s]) & 1ull)) {
-            t = ring.stile[s];
-            load = false;
-          } else {
-            while ((res >> nxt) & 1ull) ++nxt;
-            t = nxt++;
-            load = true;
-            ring.sunit[s] = u;
-            ring.stile[s] = t;
-          }
-          done |= 1ull << t;
-          // publish item k's schedule (the ring has room: consumers are at
-          // most kSlots items behind a load and kSched > kSlots)
-          if (k >= (uint32_t)kSched) {
-            while (min_consumed(B) < k - kSched + 1) __nanosleep(32);
-          }
-          if (lane == 0) {
-            B.sched[k % kSched] = (uint32_t)t | ((load ? 1u : 0u) << 8);
-            __threadfence_block();
-            st_volatile_u32(&B.published, k + 1);
-          }
-          if (!load) continue;
-          WD_PROG(9, k);
-          // slot s is free once item k - kSlots is consumed.  A monotonic
-          // counter, not an mbarrier: resident (no-load) items let either
-          // side run a full phase ahead, which parity waits cannot tell.
-          if (k >= (uint32_t)kSlots) {
-            while (min_consumed(B) < k - kSlots + 1) __nanosleep(32);
-          }
-          if (lane == 0) mbar_arrive_expect_tx(&B.full[s], kTileF * 4);
-          __syncwarp();
-          const float* src = src_slice + (uint64_t)t * kTileF;
-          float* dst = slots + (size_t)s * kSlotFloats;
-          // tiles read again by a later pass stay in L2; the last pass streams
-          const uint64_t pol = p == npass - 1 ? pol_last : pol_keep;
-          if (lane < 4) bulk_g2s(dst + lane * kQStride, src + lane * kQuarter, kQuarter * 4, &B.full[s], pol);
-        }
-      }
-    }
-  } else {
-    // ----------------------------------------------------------- consumers
-    TM_DECL
-    uint32_t k = 0, xcount = 0;
-    uint32_t loads[kSlots];
-    for (int s = 0; s < kSlots; ++s) loads[s] = 0;
-    for (uint32_t u = cid; u < nunits; u += ncl) {
-      const uint64_t ebase_slice = (uint64_t)u * block + rank * slice;
-      for (int p = 0; p < npass; ++p) {
-        if (p == 2 && lane < 16) {
-          B.wmin[warp][lane] = 0x7fffffff;
-          B.wmax[warp][lane] = (int)0x80000000;
-        }
-        if (p == 2) __syncwarp();
-        const double mu = B.mu;
-        for (int i = 0; i < T; ++i, ++k) {
-          const int s = k % kSlots;
-          if (ld_volatile_u32(&B.published) <= k) {
-            while (ld_volatile_u32(&B.published) <= k) __nanosleep(20);
-          }
-          const uint32_t e = ld_volatile_u32(&B.sched[k % kSched]);
-          const int t = (int)(e & 0xffu);
-          const bool load = (e >> 8) & 1u;
-          TM_MARK(5);
-          if (load) {
-            WD_WAIT(&B.full[s], loads[s] & 1u, 2, k, u, (p << 8) | s);
-            ++loads[s];
-          }
-          TM_MARK(0);
-          const float* sl = slots + (size_t)s * kSlotFloats;
-          if (p == 0) {
-            tile_leaf_sums<false>(sl, 0.0, B.leafsum[t]);
-          } else if (p == 1) {
-            tile_leaf_sums<true>(sl, mu, B.leafsum[t]);
-          } else if (p == 2) {
-            // labels and current extrema first (independent LDS), atomics
-            // (rare once the extrema settle) last
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              float v[8];
-#pragma unroll
-              for (int j = 0; j < 2; ++j) {
-                const float4 v4 =
-                    *reinterpret_cast<const float4*>(sl + qpad(4u * ((2 * h + j) * kBCons + tid)));
-                v[4 * j] = v4.x;
-                v[4 * j + 1] = v4.y;
-                v[4 * j + 2] = v4.z;
-                v[4 * j + 3] = v4.w;
-              }
-              uint32_t c[8];
-              int key[8];
-#pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                c[i] = label_of(B.lf, v[i]);
-                key[i] = fkey(v[i]);
-              }
-              int* wmn = B.wmin[warp];
-              int* wmx = B.wmax[warp];
-              int mn[8], mx[8];
-#pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                mn[i] = wmn[c[i]];
-                mx[i] = wmx[c[i]];
-              }
-#pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                if (key[i] < mn[i]) atomicMin(&wmn[c[i]], key[i]);
-                if (key[i] > mx[i]) atomicMax(&wmx[c[i]], key[i]);
-              }
-            }
-          } else {
-            const uint64_t ebase = ebase_slice + (uint64_t)t * kTileF;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const uint32_t e = 4u * (j * kBCons + tid);
-              const float4 v4 = *reinterpret_cast<const float4*>(sl + qpad(e));
-              const float v[4] = {v4.x, v4.y, v4.z, v4.w};
-              uint32_t c[4], code[4];
-              bool amb = false;
-#pragma unroll
-              for (int i = 0; i < 4; ++i) c[i] = label_of(B.lb, v[i]);
-#pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const float2 bp = B.qp[c[i]];
-                const float tt = __fsub_rn(__fmul_rn(__fsub_rn(v[i], bp.x), bp.y), 0.5f);
-                // the estimate is exact unless tt lies within 2^-12 of an integer
-                amb |= isnan(tt) || fabsf(__fsub_rn(tt, rintf(tt))) <= 0.000244140625f;
-                code[i] = (uint32_t)min(max(__float2int_ru(tt), 0), 255);
-              }
-              if (__builtin_expect(amb, 0)) {
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                  const float2 bp = B.qp[c[i]];
-                  const float tt = __fsub_rn(__fmul_rn(__fsub_rn(v[i], bp.x), bp.y), 0.5f);
-                  if (isnan(tt) || fabsf(__fsub_rn(tt, rintf(tt))) <= 0.000244140625f) {
-                    if (isnan(v[i])) c[i] = B.qlast;
-                    code[i] = exact_code(v[i], B.qp[c[i]].x, B.qs[c[i]]);
-                  }
-                }
-              }
-              *reinterpret_cast<uint32_t*>(codes + ebase + e) =
-                  code[0] | (code[1] << 8) | (code[2] << 16) | (code[3] << 24);
-              *reinterpret_cast<uint16_t*>(labels + (ebase + e) / 2) =
-                  (uint16_t)(c[0] | (c[1] << 4) | (c[2] << 8) | (c[3] << 12));
-            }
-          }
-          TM_MARK(1 + p);
-          __syncwarp();  // this warp's shared-memory reads of slot s are done
-          if (lane == 0) st_volatile_u32(&B.wconsumed[warp], k + 1);
-          WD_PROG(warp, k + 1);
-        }
-        // ------------------------------------------- end of pass: reduce
-        TM_MARK(5);
-        consumers_sync();
-        if (p == 3) continue;  // quantize needs no cross-CTA reduction
-        const uint32_t xb = xcount & 1u, xph = (xcount >> 1) & 1u;
-        ++xcount;
-        if (p < 2) {
-          for (int t = warp; t < T; t += kBWarps) {  // leaf sums -> tile sums
-            const double ts = tile_sum_from_leaves(B.leafsum[t], lane);
-            if (lane == 0) B.tsum[t] = ts;
-          }
-          consumers_sync();
-          if (warp == 0) {
-            if (lane == 0) {
-              B.xval[xb] = perfect_sum(B.tsum, T);
-            }
-            __syncwarp();
-            if (lane < kC) mbar_arrive_cluster(dsmem_addr(&B.xbar[xb], lane));
-            WD_WAITC(&B.xbar[xb], xph, 3, xcount, u, p);
-            double v = lane < kC ? ld_dsmem_f64(dsmem_addr(&B.xval[xb], lane)) : 0.0;
-#pragma unroll
-            for (int d = 1; d < kC; d <<= 1) v = __dadd_rn(v, __shfl_xor_sync(kFull, v, d));
-            if (lane == 0) {
-              const double sm = __ddiv_rn(__dadd_rn(0.0, v), (double)block);
-              if (p == 0) {
-                B.mu = sm;
-              } else {
-                const double m0 = B.mu, sd = __dsqrt_rn(sm);
-                B.sd = sd;
-                bsnp_cluster_table& tb = tables[u];
-                if (rank == 0) {
-                  tb.mean = __double2float_rn(m0);
-                  tb.std = __double2float_rn(sd);
-                  tb.m = (uint32_t)m;
-                  tb.flags = (isfinite(m0) && isfinite(sd)) ? 0u : BSNP_ERR_NONFINITE;
-                  for (int kk = 0; kk < 13; ++kk) tb.reserved[kk] = 0;
-                }
-                for (int kk = 0; kk < 16; ++kk) {
-                  float bf = __int_as_float(0x7f800000), br = bf;
-                  if (kk < m - 1) {
-                    const double b64 = __dadd_rn(m0, __dmul_rn(sd, kNdtri[m][kk]));
-                    bf = __double2float_rd(b64);
-                    br = __double2float_rn(b64);
-                  }
-                  B.lf.bnd[kk] = bf;
-                  B.lb.bnd[kk] = br;
-                  if (rank == 0 && kk < 15) tb.boundaries[kk] = kk < m - 1 ? br : 0.0f;
-                }
-              }
-            }
-          }
-          consumers_sync();
-          if (p == 1) {
-            // both label tables, 64 builders each (all 256 consumers join the vote)
-            lut_build(tid < 64 ? B.lf : B.lb, m, tid & 63, tid < 128);
-          }
-        } else if (p == 2) {
-          if (warp == 0) {
-            int a0 = lane < 16 ? 0x7fffffff : (int)0x80000000;
-            for (int w = 0; w < kBWarps; ++w)
-              a0 = lane < 16 ? min(a0, B.wmin[w][lane]) : max(a0, B.wmax[w][lane - 16]);
-            B.xmm[xb][lane] = a0;
-            __syncwarp();
-            if (lane < kC) mbar_arrive_cluster(dsmem_addr(&B.xbar[xb], lane));
-            WD_WAITC(&B.xbar[xb], xph, 4, xcount, u, p);
-            int a = lane < 16 ? 0x7fffffff : (int)0x80000000;
-            for (int r = 0; r < kC; ++r) {
-              const int v = ld_dsmem_s32(dsmem_addr(&B.xmm[xb][lane], r));
-              a = lane < 16 ? min(a, v) : max(a, v);
-            }
-            const int hi = __shfl_down_sync(kFull, a, 16);
-            if (lane < 16) {
-              float scale = 0.0f, offset = 0.0f;
-              if (lane < m && a <= hi) {
-                const float lo = fkey_inv(a), h = fkey_inv(hi);
-                scale = __double2float_rn(__dsub_rn((double)h, (double)lo));
-                offset = lo;
-              }
-              if (rank == 0) {
-                tables[u].scales[lane] = scale;
-                tables[u].offsets[lane] = offset;
-              }
-              float rc = 0.0f;
-              if (scale > 0.0f) {
-                rc = __fdiv_rn(255.0f, scale);
-                if (!isfinite(rc)) rc = __int_as_float(0x7fffffff);
-              }
-              B.qp[lane] = make_float2(offset, rc);
-              B.qs[lane] = scale;
-              if (lane == 0) B.qlast = (uint32_t)(m - 1);
-            }
-          }
-          consumers_sync();
-        }
-        TM_MARK(6);
-        // pass 3 needs no reduction; the next unit starts with pass 0
-      }
-    }
-  }
-  cluster_barrier();  // peers may still read this CTA's shared memory
-}
-
 // ------------------------------------------------------- precision report
 // sum (o-r)^2, sum |o-r|/|o| over |o| > 1e-12, count of such o (float64)
 __global__ void __launch_bounds__(kQThreads)
@@ -1381,76 +823,6 @@ QWs carve(const QPlan& P, void* ws) {
   return w;
 }
 
-// CTAs per thread-block cluster of the fused encoder (BSNP_QCLUSTER=2|4|8)
-int cluster_size() {
-  static const int c = [] {
-    const char* e = getenv("BSNP_QCLUSTER");
-    const int v = e ? atoi(e) : 4;
-    return (v == 4 || v == 8) ? v : 4;
-  }();
-  return c;
-}
-
-// Full units of a per-block call that the fused cluster kernel can take.
-uint64_t fused_units(uint64_t n, uint64_t block) {
-  // opt-in while the tiled kernels are faster (quantizer notes)
-  static const bool on = [] {
-    const char* e = getenv("BSNP_FUSED");
-    return e && atoi(e) != 0;
-  }();
-  if (!on) return 0;
-  if (block == 0 || block > n || (block & (block - 1))) return 0;
-  const uint64_t slice = block / cluster_size();
-  if (slice % kTileF) return 0;
-  const uint64_t T = slice / kTileF;
-  if (T < (uint64_t)kSlots || T > (uint64_t)kMaxT) return 0;
-  return n / block;
-}
-
-template <int kC>
-int launch_block_c(const float* x, uint64_t nunits, uint64_t block, int m,
-                   bsnp_cluster_table* tables, uint8_t* labels, uint8_t* codes, int do_quant,
-                   cudaStream_t s) {
-  auto k = quant_block_kernel<kC>;
-  const size_t smem = (size_t)kSlots * kSlotBytes + sizeof(BlockSmem);
-  static_assert((size_t)kSlots * kSlotBytes + sizeof(BlockSmem) <= 232448, "smem budget");
-  int rc = cuda_status("cudaFuncSetAttribute(smem)",
-                       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)smem));
-  if (rc) return rc;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = kC;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(kC, 1, 1);
-  cfg.blockDim = dim3(kBThreads, 1, 1);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  int maxc = 0;
-  rc = cuda_status("cudaOccupancyMaxActiveClusters",
-                   cudaOccupancyMaxActiveClusters(&maxc, k, &cfg));
-  if (rc) return rc;
-  if (maxc < 1) maxc = 1;
-  const uint64_t ncl = nunits < (uint64_t)maxc ? nunits : (uint64_t)maxc;
-  cfg.gridDim = dim3((unsigned)(ncl * kC), 1, 1);
-  return cuda_status("quant_block_kernel",
-                     cudaLaunchKernelEx(&cfg, k, x, (uint32_t)nunits, block, m, tables, labels,
-                                        codes, do_quant));
-}
-
-int launch_block(const float* x, uint64_t nunits, uint64_t block, int m,
-                 bsnp_cluster_table* tables, uint8_t* labels, uint8_t* codes, int do_quant,
-                 cudaStream_t s) {
-  switch (cluster_size()) {
-    case 8: return launch_block_c<8>(x, nunits, block, m, tables, labels, codes, do_quant, s);
-    default: return launch_block_c<4>(x, nunits, block, m, tables, labels, codes, do_quant, s);
-  }
-}
-
 int run_fit(const float* x, const QPlan& P, bsnp_cluster_table* tables, const QWs& w,
             cudaStream_t s) {
   int rc;
@@ -1516,24 +888,6 @@ int run_window(const float* x, const QPlan& P, bsnp_cluster_table* tables, uint8
 
 using namespace bsnp;
 
-#ifdef BSNP_WATCHDOG
-extern "C" int bsnpdbg_timing(unsigned long long* out8, int reset) {
-  cudaMemcpyFromSymbol(out8, g_tm, sizeof(g_tm));
-  if (reset) {
-    unsigned long long z[8] = {0};
-    cudaMemcpyToSymbol(g_tm, z, sizeof(z));
-  }
-  return 0;
-}
-extern "C" int bsnpdbg_progress(unsigned* out) {
-  return (int)cudaMemcpyFromSymbol(out, g_wd_prog, sizeof(g_wd_prog));
-}
-extern "C" int bsnpdbg_watchdog(unsigned long long* out, unsigned* n) {
-  cudaMemcpyFromSymbol(out, g_wd_log, sizeof(g_wd_log));
-  cudaMemcpyFromSymbol(n, g_wd_n, sizeof(unsigned));
-  return 0;
-}
-#endif
 
 extern "C" size_t bsnp_cluster_ws_bytes(uint64_t n, uint64_t block) {
   QPlan P;
@@ -1544,8 +898,8 @@ extern "C" size_t bsnp_cluster_ws_bytes(uint64_t n, uint64_t block) {
   return b;
 }
 
-// Per-block calls: full power-of-two blocks go through the fused cluster
-// kernel, the remaining tail (and every other shape) through the tiled kernels.
+// Per-block calls: full power-of-two blocks may take the resident-tile kernel
+// (opt-in); everything else, and the tail, the tiled window kernels.
 static int cluster_run(const float* x, uint64_t n, uint64_t block, int m,
                        bsnp_cluster_table* tables, uint8_t* labels, uint8_t* codes, void* ws,
                        size_t ws_bytes, cudaStream_t s) {
@@ -1569,21 +923,6 @@ static int cluster_run(const float* x, uint64_t n, uint64_t block, int m,
     } else if (rc != BSNP_E_INVALID) {
       return rc;
     }
-  }
-  const uint64_t fu = (aligned && block) ? fused_units(n, block) : 0;
-  if (fu) {
-    int rc = launch_block(x, fu, block, m, tables, labels, codes, quant ? 1 : 0, s);
-    if (rc) return rc;
-    const uint64_t done = fu * block;
-    if (done == n) return BSNP_OK;
-    x += done;
-    tables += fu;
-    if (quant) {
-      labels += done / 2;
-      codes += done;
-    }
-    n -= done;
-    block = 0;
   }
   QPlan P;
   if (!make_plan(n, block, m, P)) return BSNP_E_INVALID;

@@ -102,36 +102,6 @@ def test_per_block_vs_oracle(dev, n, block):
                               O.cluster_dequantize(p, c, xs.size, ora).view(np.uint32))
 
 
-@pytest.mark.parametrize("n,block", [(3 << 20, 1 << 20), ((1 << 21) + 1000, 1 << 19),
-                                     ((1 << 20) + 8, 1 << 19)])
-@pytest.mark.parametrize("dist", ["adam_m", "adam_v", "scaled"])
-def test_fused_cluster_kernel_vs_oracle(dev, n, block, dist):
-    """Power-of-two blocks >= 2^19 take the fused thread-block-cluster kernel
-    (tail units the tiled kernels); every unit must equal the oracle.  The
-    fused kernel is opt-in (BSNP_FUSED=1); this test runs it in a subprocess
-    environment flag set before the library reads it."""
-    import os
-    if os.environ.get("BSNP_FUSED") != "1":
-        pytest.skip("fused cluster encoder is opt-in (run with BSNP_FUSED=1)")
-    from paper_2511_12376_b200 import quantizer as Q
-    rng = np.random.default_rng(n % 1000 + len(dist))
-    x = {"adam_m": lambda: rng.standard_normal(n) * 1e-3,
-         "adam_v": lambda: (rng.standard_normal(n) * 1e-3) ** 2,
-         "scaled": lambda: rng.standard_normal(n) * 40 + 7}[dist]().astype(np.float32)
-    m = 16 if dist != "scaled" else 5
-    dq = Q.cluster_encode_device(_f32(x, dev), m, block)
-    _check_units(x, m, block, dq)
-    tables = Q.cluster_fit_device(_f32(x, dev), m, block)   # fit-only path of the kernel
-    assert bytes(tables.cpu().numpy()) == bytes(dq.tables.cpu().numpy())
-    out = Q.cluster_dequantize_device(dq).cpu().numpy()
-    for u, xs in enumerate(O.blockwise(x, block)):
-        ora = O.cluster_fit(xs, m)
-        p, c, _ = O.cluster_quantize(xs, ora)
-        s = u * block
-        assert np.array_equal(out[s:s + xs.size].view(np.uint32),
-                              O.cluster_dequantize(p, c, xs.size, ora).view(np.uint32))
-
-
 def test_fit_then_quantize_separately(dev):
     from paper_2511_12376_b200 import quantizer as Q
     x = (np.random.default_rng(4).standard_normal(70001) * 3 + 1).astype(np.float32)
