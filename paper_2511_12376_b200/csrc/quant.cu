@@ -64,8 +64,8 @@ __device__ __forceinline__ TileRef locate(const QPlan& P, uint64_t tile) {
   TileRef r;
   const uint64_t full_tiles = (uint64_t)(P.nunits - 1) * P.T_full;
   if (tile < full_tiles) {
-    r.u = (uint32_t)(tile / P.T_full);
-    r.j = (uint32_t)(tile % P.T_full);
+    r.u = (uint32_t)(tile >> P.D_full);  // T_full = 2^D_full
+    r.j = (uint32_t)(tile & (P.T_full - 1));
     r.D = P.D_full;
     r.len = P.block;
   } else {
@@ -75,6 +75,12 @@ __device__ __forceinline__ TileRef locate(const QPlan& P, uint64_t tile) {
     r.len = P.last_len;
   }
   r.ustart = (uint64_t)r.u * P.block;
+  if ((r.len & (r.len - 1)) == 0 && (r.len >> r.D) >= 16) {
+    // power-of-two unit: numpy's splits are exact halves
+    r.size = r.len >> r.D;
+    r.off = (uint64_t)r.j * r.size;
+    return r;
+  }
   uint64_t off = 0, size = r.len;
   for (int b = (int)r.D - 1; b >= 0; --b) {
     const uint64_t L = 8 * (size / 16);
@@ -446,7 +452,7 @@ __global__ void __launch_bounds__(kQThreads)
   // pass left undecided are visited (a small grid skips the rest quickly)
   for (uint64_t tile = blockIdx.x; tile < P.total_tiles; tile += gridDim.x) {
     if (need) {
-      const uint32_t uu = tile < full_tiles ? (uint32_t)(tile / P.T_full) : P.nunits - 1;
+      const uint32_t uu = tile < full_tiles ? (uint32_t)(tile >> P.D_full) : P.nunits - 1;
       if (!need[uu]) continue;
     }
     const TileRef r = locate(P, tile);
