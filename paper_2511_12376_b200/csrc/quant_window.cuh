@@ -24,10 +24,11 @@
 // lo <= F_k exists, every element in (lo, F_k] has label k and lies within
 // delta, so it is a candidate too: lo is pred(F_k).  Likewise for succ
 // (elements in (F_k, hi) have label k+1, or equal B32_k > F_k with label k).
-// delta = 160 sd / n: for dense data pred/succ are ~sd/(n pdf) away, so a
-// missing side (probability ~e^-19 per threshold) only costs the exact round.
-constexpr uint32_t kWDeltaNum = 160;
-constexpr int kWBins = 4096;            // label LUT bins over mu +- 2 sd
+// delta = 80 sd / n: for dense data pred/succ are ~sd/(n pdf) away (<= 8.3
+// sd / n for every threshold of m <= 16), so a missing side (probability
+// <= e^-9.6 per threshold side) only costs the exact round of that unit.
+constexpr uint32_t kWDeltaNum = 80;
+constexpr int kWBins = 16384;           // label LUT bins over mu +- 2 sd
 constexpr uint32_t kLutN = 0x40u;       // LUT bit: the bin meets some [F_k - delta, F_k + delta]
 
 __device__ __forceinline__ uint32_t w_bin(float v, float gi, float c0) {
@@ -51,6 +52,7 @@ static_assert(sizeof(UGrid) % 16 == 0, "UGrid alignment");
 __global__ void __launch_bounds__(kQThreads)
     fit_grid_kernel(QPlan P, const double* __restrict__ mu, const double* __restrict__ sdv,
                     const bsnp_cluster_table* __restrict__ tables, UGrid* __restrict__ ug) {
+  __shared__ __align__(16) uint8_t lut[kWBins];
   __shared__ int binB[16], nlo[16], nhi[16];
   __shared__ float s_gi, s_c0, s_delta;
   __shared__ uint32_t s_mode;
@@ -104,24 +106,31 @@ __global__ void __launch_bounds__(kQThreads)
     s_mode = mode;
     G.mode = mode;
   }
-  __syncthreads();
-  // thread t: bins [16t, 16t + 16)
-  static_assert(kWBins == 16 * kQThreads, "16 LUT bins per thread");
-  const int b0 = 16 * tid;
+  // thread t: bins [64t, 64t + 64): L = #boundaries in lower bins, kLutB
+  constexpr int kPer = kWBins / kQThreads;
+  const int b0 = kPer * tid;
   int cnt = 0;
   for (int k = 0; k < m - 1; ++k) cnt += binB[k] < b0;
-  uint32_t w[4] = {0, 0, 0, 0};
+  for (int q = 0; q < kPer; q += 4) {
+    uint32_t w = 0;
 #pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    const int bb = b0 + q;
-    while (cnt < m - 1 && binB[cnt] < bb) ++cnt;
-    uint32_t e = (uint32_t)cnt;
-    if (cnt < m - 1 && binB[cnt] == bb) e |= kLutB;
-    for (int k = 0; k < m - 1; ++k)
-      if (nlo[k] <= bb && bb <= nhi[k]) e |= kLutN;
-    w[q >> 2] |= e << (8 * (q & 3));
+    for (int qq = 0; qq < 4; ++qq) {
+      const int bb = b0 + q + qq;
+      while (cnt < m - 1 && binB[cnt] < bb) ++cnt;
+      uint32_t e = (uint32_t)cnt;
+      if (cnt < m - 1 && binB[cnt] == bb) e |= kLutB;
+      w |= e << (8 * qq);
+    }
+    *reinterpret_cast<uint32_t*>(&lut[b0 + q]) = w;
   }
-  reinterpret_cast<uint4*>(G.lut)[tid] = make_uint4(w[0], w[1], w[2], w[3]);
+  __syncthreads();
+  // threshold windows (disjoint for any usable grid; overlaps only set a bit
+  // twice)
+  for (int k = 0; k < m - 1; ++k)
+    for (int bb = nlo[k] + tid; bb <= nhi[k]; bb += kQThreads) lut[bb] |= (uint8_t)kLutN;
+  __syncthreads();
+  for (int i = tid; i < kWBins / 16; i += kQThreads)
+    reinterpret_cast<uint4*>(G.lut)[i] = reinterpret_cast<const uint4*>(lut)[i];
 }
 
 // elementwise passes run over kDqChunk-element chunks of each unit (the
@@ -219,17 +228,24 @@ __device__ __forceinline__ void w_label_loop(WSmem& S, const float* src, uint32_
       }
       vmin = fmin3(vmin, fminf(v[0], v[1]), fminf(v[2], v[3]));
       vmax = fmax3(vmax, fmaxf(v[0], v[1]), fmaxf(v[2], v[3]));
-      // rare (~1 % of elements): a quantize boundary inside the bin, or a fit
-      // threshold near; each slot is handled only if some lane of the warp
-      // needs it, so the common warp skips the per-slot work
-      const unsigned act = __activemask();
-      if (__any_sync(act, ((le[0] | le[1] | le[2] | le[3]) & (kLutB | kLutN)) != 0)) {
+      // rare (~0.3 % of elements): a quantize boundary inside the bin, or a
+      // fit threshold near; each lane walks only its own flagged slots
+      uint32_t spec = 0;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          if (!__any_sync(act, (le[q] & (kLutB | kLutN)) != 0)) continue;
-          if (!kCmp && (le[q] & kLutB)) c[q] += v[q] > S.B32[c[q]] ? 1u : 0u;
-          if ((le[q] & kLutN) && w_near(S, v[q], c[q])) w_candidates(S, v[q], c[q], m);
-        }
+      for (int q = 0; q < 4; ++q) spec |= (le[q] & (kLutB | kLutN)) ? (1u << q) : 0u;
+      if (__builtin_expect(spec != 0, 0)) {
+        auto fix = [&](float vq, uint32_t leq, uint32_t& cq) {
+          if (!kCmp && (leq & kLutB)) cq += vq > S.B32[cq] ? 1u : 0u;
+          if ((leq & kLutN) && w_near(S, vq, cq)) w_candidates(S, vq, cq, m);
+        };
+        do {
+          const int q = __ffs(spec) - 1;
+          spec &= spec - 1;
+          if (q == 0) fix(v[0], le[0], c[0]);
+          else if (q == 1) fix(v[1], le[1], c[1]);
+          else if (q == 2) fix(v[2], le[2], c[2]);
+          else fix(v[3], le[3], c[3]);
+        } while (spec);
       }
       if (lab)
         *reinterpret_cast<uint16_t*>(lab + 2 * i) =
@@ -258,7 +274,8 @@ __global__ void __launch_bounds__(kQThreads)
   const ChunkRef r = chunk_of(P, blockIdx.x);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, m = (int)P.m;
   UGrid& G = ug[r.u];
-  reinterpret_cast<uint4*>(S.lut)[tid] = reinterpret_cast<const uint4*>(G.lut)[tid];
+  for (int i = tid; i < kWBins / 16; i += kQThreads)
+    reinterpret_cast<uint4*>(S.lut)[i] = reinterpret_cast<const uint4*>(G.lut)[i];
   if (tid < 16) {
     const float f = G.F[tid];
     S.F[tid] = f;
