@@ -659,6 +659,82 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// In-place apply for chain replay (store.py:441-454): only the changed
+// elements are written.  Persistent grid over tiles; thread t owns the 32
+// elements of mask word t of the tile (one u32 load), so the work per
+// element is one bit test and the scatter is a loop over set bits only.
+// Runs after delta_offsets_kernel validated the mask (never when a flag is
+// raised, so a corrupt record leaves the base untouched).
+__global__ void __launch_bounds__(kThreads)
+    delta_apply_inplace_kernel(const uint8_t* __restrict__ mask,
+                               const uint16_t* __restrict__ payload, uint64_t n, uint64_t n_c,
+                               uint16_t* out, const uint64_t* __restrict__ offsets,
+                               const bsnp_status* __restrict__ st) {
+  __shared__ uint32_t s_warp[kWarps];
+  if (*(volatile const uint32_t*)&st->err_flags) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t ntiles = (n + kTile - 1) / kTile;
+  const uint64_t nbytes = (n + 7) / 8;
+  const bool aligned = ((uintptr_t)mask & 3) == 0;
+  const bool vec_out = ((uintptr_t)out & 15) == 0;
+  // thread t owns mask word t of the tile (32 elements); the next tile's
+  // word is loaded before this one is processed (two loads in flight)
+  auto load_word = [&](uint64_t tile) -> uint32_t {
+    const uint64_t b0 = tile * kMaskBytes + 4 * (uint64_t)tid;
+    uint32_t w = 0;
+    if (b0 + 4 <= nbytes && aligned) {
+      w = __ldg(reinterpret_cast<const uint32_t*>(mask + b0));
+    } else {
+      for (uint32_t i = 0; i < 4 && b0 + i < nbytes; ++i)
+        w |= (uint32_t)__ldg(mask + b0 + i) << (8 * i);
+    }
+    const uint64_t e0 = b0 * 8;
+    if (e0 + 32 > n) w &= e0 >= n ? 0u : (0xffffffffu >> (32 - (uint32_t)(n - e0)));
+    return w;
+  };
+  uint64_t tile = blockIdx.x;
+  uint32_t w_next = tile < ntiles ? load_word(tile) : 0u;
+  for (; tile < ntiles; tile += gridDim.x) {
+    uint32_t w = w_next;
+    if (tile + gridDim.x < ntiles) w_next = load_word(tile + gridDim.x);
+    const uint64_t e0 = (tile * kMaskBytes + 4 * (uint64_t)tid) * 8;
+    const uint32_t c = __popc(w);
+    const uint32_t inc = warp_inclusive_scan_u32(c, lane);
+    if (lane == 31) s_warp[warp] = inc;
+    __syncthreads();
+    uint32_t before = 0;
+#pragma unroll
+    for (int i = 0; i < kWarps; ++i) before += i < warp ? s_warp[i] : 0u;
+    __syncthreads();  // s_warp is reused by the next tile
+    uint64_t pos = offsets[tile] + before + inc - c;
+    if (c >= 4 && e0 + 32 <= n && vec_out) {
+      // dense word: read-modify-write its 64 bytes with vector accesses
+      // (32 scattered 2-byte stores per warp instruction cost more)
+      uint4* o4 = reinterpret_cast<uint4*>(out + e0);
+      uint4 v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[q] = o4[q];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        if ((w >> k) & 1u) {
+          const uint32_t val = pos < n_c ? (uint32_t)payload[pos] : 0u;
+          set_u16_lane(v[k >> 3], (uint32_t)(k & 7), val);
+          ++pos;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) o4[q] = v[q];
+    } else {
+      while (w) {
+        const uint32_t k = __ffs(w) - 1;
+        w &= w - 1;
+        if (pos < n_c) out[e0 + k] = payload[pos];
+        ++pos;
+      }
+    }
+  }
+}
+
 // persistent grid size for a dynamic-smem kernel
 template <typename K>
 int persistent_grid(K kernel, size_t smem, uint64_t work_items, int threads = kThreads) {
@@ -771,8 +847,15 @@ extern "C" int bsnp_delta_decode(const uint16_t* base, const uint8_t* mask,
   const bool in_place = (const void*)base == (const void*)out;
   const bool aligned = (((uintptr_t)base | (uintptr_t)out | (uintptr_t)mask) & 15) == 0;
   if (in_place) {
-    delta_apply_kernel<true><<<(unsigned)nt, kThreads, 0, s>>>(base, mask, payload, n, n_c,
-                                                                out, offsets, status);
+    static int sms = 0;
+    if (!sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const uint64_t grid = nt < (uint64_t)sms * 8 ? nt : (uint64_t)sms * 8;
+    delta_apply_inplace_kernel<<<(unsigned)grid, kThreads, 0, s>>>(mask, payload, n, n_c, out,
+                                                                   offsets, status);
   } else if (aligned) {
     const size_t smem = (size_t)kDecStages * kDecStage;
     auto k = delta_decode_tma_kernel<kDecStages>;
