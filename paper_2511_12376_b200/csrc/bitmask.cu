@@ -486,7 +486,7 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-template <int kStages>
+template <int kStages, bool kDense>
 __global__ void __launch_bounds__(kThreads)
     delta_decode_tma_kernel(const uint16_t* __restrict__ base, const uint8_t* __restrict__ mask,
                             const uint16_t* __restrict__ payload, uint64_t n, uint64_t n_c,
@@ -588,20 +588,34 @@ __global__ void __launch_bounds__(kThreads)
     for (int j = 0; j < kVec; ++j) cnt[j] = __popc(bits[j]);
     tile_local_scan(cnt, off, s_warp, s_off);
     const uint16_t* sp = reinterpret_cast<const uint16_t*>(stage + kTileBytes + kMaskBytes);
+
 #pragma unroll
     for (int j = 0; j < kVec; ++j) {
       uint32_t b = bits[j];
       uint32_t r = off[j];
       uint4 v = bv[j];
-      while (b) {
-        const uint32_t k = __ffs(b) - 1;
-        b &= b - 1;
-        const uint64_t pos = poff + r;
-        uint32_t val;
-        if (shift != ~0u) val = sp[shift + r];
-        else val = pos < n_c ? payload[pos] : 0u;
-        set_u16_lane(v, k, val);
-        ++r;
+      auto fetch = [&](uint32_t rr) -> uint32_t {
+        const uint64_t pos = poff + rr;
+        if (shift != ~0u) return sp[shift + rr];
+        return pos < n_c ? payload[pos] : 0u;
+      };
+      if (kDense) {
+        // dense records (n_c > n/32, chosen on the host): expand with static
+        // lane indices instead of walking the set bits
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          if ((b >> k) & 1u) {
+            set_u16_lane(v, (uint32_t)k, fetch(r));
+            ++r;
+          }
+        }
+      } else {
+        while (b) {
+          const uint32_t k = __ffs(b) - 1;
+          b &= b - 1;
+          set_u16_lane(v, k, fetch(r));
+          ++r;
+        }
       }
       const uint64_t e = t0 + (uint64_t)(j * kThreads + tid) * 8;
       if (full) {
@@ -735,21 +749,32 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-// persistent grid size for a dynamic-smem kernel
+// persistent grid size for a dynamic-smem kernel (attribute + occupancy
+// query once per kernel and thread: they cost microseconds per call)
 template <typename K>
 int persistent_grid(K kernel, size_t smem, uint64_t work_items, int threads = kThreads) {
-  static int sms = -1;
-  if (sms < 0) {
-    int dev = 0;
+  struct Entry {
+    const void* fn;
+    size_t smem;
+    int threads;
+    int blocks;
+  };
+  thread_local Entry cache[8];
+  thread_local int used = 0;
+  int blocks = 0;
+  for (int i = 0; i < used; ++i)
+    if (cache[i].fn == (const void*)kernel && cache[i].smem == smem && cache[i].threads == threads)
+      blocks = cache[i].blocks;
+  if (!blocks) {
+    int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+    blocks = sms * (per_sm < 1 ? 1 : per_sm);
+    if (used < 8) cache[used++] = Entry{(const void*)kernel, smem, threads, blocks};
   }
-  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
-  if (per_sm < 1) per_sm = 1;
-  uint64_t g = (uint64_t)sms * per_sm;
-  if (g > work_items) g = work_items;
+  const uint64_t g = (uint64_t)blocks < work_items ? (uint64_t)blocks : work_items;
   return (int)(g ? g : 1);
 }
 
@@ -858,7 +883,8 @@ extern "C" int bsnp_delta_decode(const uint16_t* base, const uint8_t* mask,
                                                                    offsets, status);
   } else if (aligned) {
     const size_t smem = (size_t)kDecStages * kDecStage;
-    auto k = delta_decode_tma_kernel<kDecStages>;
+    auto k = n_c * 32 > n ? delta_decode_tma_kernel<kDecStages, true>
+                          : delta_decode_tma_kernel<kDecStages, false>;
     const int grid = persistent_grid(k, smem, nt);
     k<<<grid, kThreads, smem, s>>>(base, mask, payload, n, n_c, out, offsets, ticket2);
   } else {
