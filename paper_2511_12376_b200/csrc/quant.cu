@@ -167,11 +167,12 @@ __device__ void lut_build_cta(LabelLut& L, int m) {
 }
 
 // Load elements [0, size) of a tile into padded shared memory.
-__device__ __forceinline__ void load_tile(float* s, const float* src, uint32_t size) {
+__device__ __forceinline__ void load_tile(float* s, const float* src, uint32_t size,
+                                          uint64_t pol) {
   if (((uintptr_t)src & 15) == 0) {
     const uint32_t nv = size / 4;
     for (uint32_t v = threadIdx.x; v < nv; v += blockDim.x) {
-      const float4 x = ld_stream_f4(src + 4 * v);
+      const float4 x = ld_hint_f4(src + 4 * v, pol);
       *reinterpret_cast<float4*>(&s[padded(4 * v)]) = x;
     }
     for (uint32_t i = nv * 4 + threadIdx.x; i < size; i += blockDim.x) s[padded(i)] = src[i];
@@ -267,15 +268,14 @@ __device__ double tree_sum(const float* s, uint32_t size, double mu, Heap& H) {
 // perfect 8192-element tiles: 8 floats of padding per 1024 (8 leaves)
 __device__ __forceinline__ uint32_t epad(uint32_t e) { return e + ((e >> 10) << 3); }
 
+// The pairwise sum of one tree tile (a depth-D node); the result is valid in
+// thread 0.  s / H are the tile's shared-memory staging and heap.
 template <bool kVar>
-__global__ void __launch_bounds__(kQThreads)
-    fit_tree_kernel(const float* __restrict__ x, QPlan P, const double* __restrict__ mu,
-                    double* __restrict__ partials) {
-  __shared__ __align__(16) float s[kSmemFloats];
-  __shared__ Heap H;
-  const TileRef r = locate(P, blockIdx.x);
+__device__ __forceinline__ double tree_tile(const float* __restrict__ x, const QPlan& P,
+                                            uint64_t tile, double m, float* s, Heap& H,
+                                            uint64_t pol) {
+  const TileRef r = locate(P, tile);
   const float* src = x + r.ustart + r.off;
-  const double m = kVar ? mu[r.u] : 0.0;
   if (r.size == kTileMax && ((uintptr_t)src & 15) == 0) {
     // a perfect sub-tree: 64 leaves of 128.  8 lanes per leaf (lane j owns
     // numpy's accumulator r[j]); the 4 lane groups of a warp take leaves
@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(kQThreads)
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const uint32_t v = i * kQThreads + tid;
-      *reinterpret_cast<float4*>(&s[epad(4 * v)]) = ld_stream_f4(src + 4 * v);
+      *reinterpret_cast<float4*>(&s[epad(4 * v)]) = ld_hint_f4(src + 4 * v, pol);
     }
     __syncthreads();
     const int j = lane & 7, q = lane >> 3;
@@ -304,17 +304,27 @@ __global__ void __launch_bounds__(kQThreads)
       if (j == 0) H.val[leaf] = acc;
     }
     __syncthreads();
+    double v = 0.0;
     if (warp == 0) {
-      double v = __dadd_rn(H.val[2 * lane], H.val[2 * lane + 1]);
+      v = __dadd_rn(H.val[2 * lane], H.val[2 * lane + 1]);
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) v = __dadd_rn(v, __shfl_xor_sync(kFull, v, d));
-      if (lane == 0) partials[blockIdx.x] = v;
     }
-    return;
+    return v;
   }
-  load_tile(s, src, (uint32_t)r.size);
+  load_tile(s, src, (uint32_t)r.size, pol);
   __syncthreads();
-  const double v = tree_sum<kVar>(s, (uint32_t)r.size, m, H);
+  return tree_sum<kVar>(s, (uint32_t)r.size, m, H);
+}
+
+template <bool kVar>
+__global__ void __launch_bounds__(kQThreads)
+    fit_tree_kernel(const float* __restrict__ x, QPlan P, const double* __restrict__ mu,
+                    double* __restrict__ partials) {
+  __shared__ __align__(16) float s[kSmemFloats];
+  __shared__ Heap H;
+  const double m = kVar ? mu[locate(P, blockIdx.x).u] : 0.0;
+  const double v = tree_tile<kVar>(x, P, blockIdx.x, m, s, H, policy_evict_first());
   if (threadIdx.x == 0) partials[blockIdx.x] = v;
 }
 
@@ -330,7 +340,7 @@ __device__ double combine_perfect(const double* p, uint32_t T, double* sv) {
     uint32_t lvl[20];
     int top = 0;
     for (uint32_t i = 0; i < chunk; ++i) {
-      double v = c[i];
+      double v = __ldcg(c + i);
       uint32_t l = 0;
       while (top > 0 && lvl[top - 1] == l) {
         v = __dadd_rn(stk[top - 1], v);
@@ -361,13 +371,13 @@ __device__ __forceinline__ void unit_shape(const QPlan& P, uint32_t u, uint32_t&
   len = last ? P.last_len : P.block;
 }
 
+// Mean (kVar = false) or std + table header + fit thresholds (kVar = true) of
+// unit u from its tile partials; CTA-wide (sv: kQThreads doubles of smem).
 template <bool kVar>
-__global__ void __launch_bounds__(kQThreads)
-    fit_combine_kernel(QPlan P, const double* __restrict__ partials, double* __restrict__ mu,
-                       float* __restrict__ fthr, bsnp_cluster_table* __restrict__ tables,
-                       double* __restrict__ sdv = nullptr) {
-  __shared__ double sv[kQThreads];
-  const uint32_t u = blockIdx.x;
+__device__ __forceinline__ void combine_unit(const QPlan& P, uint32_t u,
+                                             const double* partials, double* mu, float* fthr,
+                                             bsnp_cluster_table* tables, double* sdv,
+                                             double* sv) {
   uint32_t T;
   uint64_t len;
   unit_shape(P, u, T, len);
@@ -379,7 +389,7 @@ __global__ void __launch_bounds__(kQThreads)
     mu[u] = mean;
     return;
   }
-  const double m0 = mu[u];
+  const double m0 = __ldcg(mu + u);
   const double var = __ddiv_rn(__dadd_rn(0.0, S), (double)len);
   const double sd = __dsqrt_rn(var);  // np.std, ddof = 0
   if (sdv) sdv[u] = sd;
@@ -400,6 +410,15 @@ __global__ void __launch_bounds__(kQThreads)
   }
   fthr[u * 16 + 15] = __int_as_float(0x7f800000);
   for (int k = 0; k < 13; ++k) tb.reserved[k] = 0;
+}
+
+template <bool kVar>
+__global__ void __launch_bounds__(kQThreads)
+    fit_combine_kernel(QPlan P, const double* __restrict__ partials, double* __restrict__ mu,
+                       float* __restrict__ fthr, bsnp_cluster_table* __restrict__ tables,
+                       double* __restrict__ sdv = nullptr) {
+  __shared__ double sv[kQThreads];
+  combine_unit<kVar>(P, blockIdx.x, partials, mu, fthr, tables, sdv, sv);
 }
 
 template <bool kLut>
@@ -871,7 +890,7 @@ int run_window(const float* x, const QPlan& P, bsnp_cluster_table* tables, uint8
   fit_combine_kernel<true><<<P.nunits, kQThreads, 0, s>>>(P, w.partials, w.mu, w.fthr, tables,
                                                            w.sd);
   if ((rc = launch_status("fit_combine_kernel<std>"))) return rc;
-  fit_grid_kernel<<<P.nunits, kQThreads, 0, s>>>(P, w.mu, w.sd, tables, w.ug);
+  fit_grid_kernel<<<P.nunits, kQThreads, 0, s>>>(P, w.mu, w.sd, w.ug);
   if ((rc = launch_status("fit_grid_kernel"))) return rc;
   const unsigned chunks = (unsigned)((uint64_t)(P.nunits - 1) * P.C_full + P.C_last);
   fit_label_kernel<<<chunks, kQThreads, 0, s>>>(x, P, w.ug, labels);

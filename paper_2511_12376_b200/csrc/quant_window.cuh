@@ -49,17 +49,22 @@ struct UGrid {
 constexpr size_t kUGridBytes = sizeof(UGrid);
 static_assert(sizeof(UGrid) % 16 == 0, "UGrid alignment");
 
-__global__ void __launch_bounds__(kQThreads)
-    fit_grid_kernel(QPlan P, const double* __restrict__ mu, const double* __restrict__ sdv,
-                    const bsnp_cluster_table* __restrict__ tables, UGrid* __restrict__ ug) {
-  __shared__ __align__(16) uint8_t lut[kWBins];
-  __shared__ int binB[16], nlo[16], nhi[16];
-  __shared__ float s_gi, s_c0, s_delta;
-  __shared__ uint32_t s_mode;
-  const uint32_t u = blockIdx.x;
+struct GridSmem {
+  __align__(16) uint8_t lut[kWBins];
+  int binB[16], nlo[16], nhi[16];
+  float s_gi, s_c0, s_delta;
+  uint32_t s_mode;
+};
+
+// CTA-wide: the bin grid, label LUT and threshold window of unit u
+__device__ __forceinline__ void grid_unit(const QPlan& P, uint32_t u, double m0, double sd,
+                                          UGrid* ug, GridSmem& g) {
+  uint8_t* lut = g.lut;
+  int *binB = g.binB, *nlo = g.nlo, *nhi = g.nhi;
+  float &s_gi = g.s_gi, &s_c0 = g.s_c0, &s_delta = g.s_delta;
+  uint32_t& s_mode = g.s_mode;
   const int tid = threadIdx.x, m = (int)P.m;
   UGrid& G = ug[u];
-  const double m0 = mu[u], sd = sdv[u];
   uint32_t T;
   uint64_t len;
   unit_shape(P, u, T, len);
@@ -133,6 +138,13 @@ __global__ void __launch_bounds__(kQThreads)
     reinterpret_cast<uint4*>(G.lut)[i] = reinterpret_cast<const uint4*>(lut)[i];
 }
 
+__global__ void __launch_bounds__(kQThreads)
+    fit_grid_kernel(QPlan P, const double* __restrict__ mu, const double* __restrict__ sdv,
+                    UGrid* __restrict__ ug) {
+  __shared__ GridSmem g;
+  grid_unit(P, blockIdx.x, mu[blockIdx.x], sdv[blockIdx.x], ug, g);
+}
+
 // elementwise passes run over kDqChunk-element chunks of each unit (the
 // dequantize partition), not the pairwise-tree tiles
 struct ChunkRef {
@@ -203,7 +215,8 @@ __device__ __forceinline__ void w_candidates(WSmem& S, float v, uint32_t c, int 
 
 template <bool kCmp>
 __device__ __forceinline__ void w_label_loop(WSmem& S, const float* src, uint32_t size,
-                                             uint8_t* lab, int m, float& vmin, float& vmax) {
+                                             uint8_t* lab, int m, float& vmin, float& vmax,
+                                             uint64_t pol) {
   const int tid = threadIdx.x;
   const bool vec = ((((uintptr_t)src) & 15) | (((uintptr_t)lab) & 1)) == 0;
   const uint32_t nv = vec ? size / 4 : 0;
@@ -213,7 +226,7 @@ __device__ __forceinline__ void w_label_loop(WSmem& S, const float* src, uint32_
 #pragma unroll
     for (int b = 0; b < kB; ++b) {
       const uint32_t i = i0 + b * kQThreads;
-      if (i < nv) v4[b] = ld_stream_f4(src + 4 * i);
+      if (i < nv) v4[b] = ld_hint_f4(src + 4 * i, pol);
     }
 #pragma unroll
     for (int b = 0; b < kB; ++b) {
@@ -267,35 +280,36 @@ __device__ __forceinline__ void w_label_loop(WSmem& S, const float* src, uint32_
   }
 }
 
-__global__ void __launch_bounds__(kQThreads)
-    fit_label_kernel(const float* __restrict__ x, QPlan P, UGrid* __restrict__ ug,
-                     uint8_t* __restrict__ labels) {
-  __shared__ __align__(16) WSmem S;
-  const ChunkRef r = chunk_of(P, blockIdx.x);
+// CTA-wide: labels + threshold-window candidates + extremes of one chunk
+// (the unit's grid is read with L2 loads: it may come from another CTA of the
+// same launch in the pipelined encoder)
+__device__ __forceinline__ void label_chunk(const float* __restrict__ x, const QPlan& P,
+                                            const ChunkRef& r, UGrid* ug, uint8_t* labels,
+                                            WSmem& S, uint64_t pol) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, m = (int)P.m;
   UGrid& G = ug[r.u];
   for (int i = tid; i < kWBins / 16; i += kQThreads)
-    reinterpret_cast<uint4*>(S.lut)[i] = reinterpret_cast<const uint4*>(G.lut)[i];
+    reinterpret_cast<uint4*>(S.lut)[i] = __ldcg(reinterpret_cast<const uint4*>(G.lut) + i);
   if (tid < 16) {
-    const float f = G.F[tid];
+    const float f = __ldcg(G.F + tid);
     S.F[tid] = f;
-    S.B32[tid] = G.B32[tid];
-    S.FF[tid] = make_float2(tid > 0 ? G.F[tid - 1] : __int_as_float(0xff800000), f);
+    S.B32[tid] = __ldcg(G.B32 + tid);
+    S.FF[tid] = make_float2(tid > 0 ? __ldcg(G.F + tid - 1) : __int_as_float(0xff800000), f);
     S.lo[tid] = 0;
     S.hi_c[tid] = 0;
   }
   if (tid == 0) {
-    S.gi = G.gi;
-    S.c0 = G.c0;
-    S.delta = G.delta;
-    S.mode = G.mode;
+    S.gi = __ldcg(&G.gi);
+    S.c0 = __ldcg(&G.c0);
+    S.delta = __ldcg(&G.delta);
+    S.mode = __ldcg(&G.mode);
   }
   __syncthreads();
   const float* src = x + r.ustart + r.c0;
   uint8_t* lab = labels ? labels + (uint64_t)r.u * (P.block / 2) + r.c0 / 2 : nullptr;
   float vmin = __int_as_float(0x7f800000), vmax = __int_as_float(0xff800000);
-  if (S.mode & 2u) w_label_loop<true>(S, src, (uint32_t)r.len, lab, m, vmin, vmax);
-  else w_label_loop<false>(S, src, (uint32_t)r.len, lab, m, vmin, vmax);
+  if (S.mode & 2u) w_label_loop<true>(S, src, (uint32_t)r.len, lab, m, vmin, vmax, pol);
+  else w_label_loop<false>(S, src, (uint32_t)r.len, lab, m, vmin, vmax, pol);
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) {
     vmin = fminf(vmin, __shfl_xor_sync(kFull, vmin, d));
@@ -321,58 +335,106 @@ __global__ void __launch_bounds__(kQThreads)
   }
 }
 
-// one warp per unit: extremes from the candidates, or mark the exact round
-__global__ void __launch_bounds__(32)
-    fit_decide_kernel(QPlan P, const UGrid* __restrict__ ug,
-                      bsnp_cluster_table* __restrict__ tables, uint32_t* __restrict__ need) {
-  const uint32_t u = blockIdx.x;
-  const int lane = threadIdx.x, m = (int)P.m;
+__global__ void __launch_bounds__(kQThreads)
+    fit_label_kernel(const float* __restrict__ x, QPlan P, UGrid* __restrict__ ug,
+                     uint8_t* __restrict__ labels) {
+  __shared__ __align__(16) WSmem S;
+  label_chunk(x, P, chunk_of(P, blockIdx.x), ug, labels, S, policy_evict_first());
+}
+
+// one warp per unit: extremes from the candidates, or mark the exact round;
+// returns ok (warp-uniform).
+//
+// Per fit threshold F_k (lane k): pred = the largest element <= F_k, succ =
+// the smallest element > F_k (ukeys, 0 = none).  With the unit extremes
+// gmin / gmax known exactly: F_k < gmin has no pred and succ = gmin; F_k >=
+// gmax has pred = gmax and no succ (thresholds outside the data, e.g. the
+// lower tail of a one-sided Adam v); otherwise both exist and the window
+// candidates must hold them (else the exact round).  Cluster c then has min =
+// succ(F_{c-1}) (gmin for c = 0) and max = pred(F_c) (gmax for c = m-1), and
+// is empty (scale = offset = 0, quantizer.py:117-125) when those fall outside
+// (F_{c-1}, F_c].  A constant unit (gmin == gmax) is decided directly.
+__device__ __forceinline__ bool decide_unit(const QPlan& P, uint32_t u, const UGrid* ug,
+                                            bsnp_cluster_table* tables, uint32_t* need) {
+  const int lane = threadIdx.x & 31, m = (int)P.m;
   const UGrid& G = ug[u];
   bsnp_cluster_table& tb = tables[u];
-  bool ok = !(G.mode & 1u);
-  uint32_t lo = 0, hic = 0;
+  const uint32_t kgmin = ~__ldcg(&G.gmin_c), kgmax = __ldcg(&G.gmax);
+  const float gmin = ukey_inv(kgmin), gmax = ukey_inv(kgmax);
+  const bool finite = kgmax != 0 && isfinite(gmin) && isfinite(gmax);
+  bool ok = finite && (!(__ldcg(&G.mode) & 1u) || kgmin == kgmax);
+  const float inf = __int_as_float(0x7f800000);
+  const float f = lane < m - 1 ? __ldcg(G.F + lane) : inf;
+  uint32_t pk = 0, sk = 0;
   if (lane < m - 1) {
-    lo = G.lo[lane];
-    hic = G.hi_c[lane];
-    ok = ok && lo != 0 && hic != 0;
+    if (f < gmin) {
+      sk = kgmin;
+    } else if (f >= gmax) {
+      pk = kgmax;
+    } else {
+      pk = __ldcg(G.lo + lane);
+      const uint32_t hc = __ldcg(G.hi_c + lane);
+      sk = hc ? ~hc : 0u;
+      ok = ok && pk != 0 && sk != 0;
+    }
   }
   ok = __all_sync(kFull, ok);
-  const uint32_t hic_prev = __shfl_up_sync(kFull, hic, 1);
+  const uint32_t sk_prev = __shfl_up_sync(kFull, sk, 1);
+  const float f_prev = __shfl_up_sync(kFull, f, 1);
   if (lane == 0) need[u] = ok ? 0u : 1u;
-  if (!ok || lane >= 16) return;
+  if (!ok || lane >= 16) return ok;
   const int c = lane;
   float scale = 0.0f, offset = 0.0f;
   if (c < m) {
-    const uint32_t kmin = c == 0 ? ~G.gmin_c : ~hic_prev;
-    const uint32_t kmax = c == m - 1 ? G.gmax : lo;
-    const float a = ukey_inv(kmin), b = ukey_inv(kmax);
-    scale = __double2float_rn(__dsub_rn((double)b, (double)a));
-    offset = a;
+    const float lo_f = c == 0 ? -inf : f_prev;  // cluster c is (lo_f, hi_f]
+    const float hi_f = c == m - 1 ? inf : f;
+    const uint32_t kmin = c == 0 ? kgmin : sk_prev;
+    const uint32_t kmax = c == m - 1 ? kgmax : pk;
+    if (kmin && kmax) {
+      const float a = ukey_inv(kmin), b = ukey_inv(kmax);
+      if (a <= hi_f && b > lo_f) {
+        scale = __double2float_rn(__dsub_rn((double)b, (double)a));
+        offset = a;
+      }
+    }
   }
   tb.scales[c] = scale;
   tb.offsets[c] = offset;
+  return ok;
+}
+
+__global__ void __launch_bounds__(32)
+    fit_decide_kernel(QPlan P, const UGrid* __restrict__ ug,
+                      bsnp_cluster_table* __restrict__ tables, uint32_t* __restrict__ need) {
+  decide_unit(P, blockIdx.x, ug, tables, need);
 }
 
 // codes of one chunk from x and its written labels (quantizer.py:174-182).
 // Labels are only read here: a NaN element keeps the label of stage C (its
 // unit is non-finite and the host raises QuantizerError).
-__global__ void __launch_bounds__(kQThreads)
-    quantize_codes_kernel(const float* __restrict__ x, QPlan P,
-                          const bsnp_cluster_table* __restrict__ tables,
-                          const uint8_t* __restrict__ labels, uint8_t* __restrict__ codes) {
-  __shared__ float2 qp[16];
-  __shared__ float qs[16];
-  const ChunkRef r = chunk_of(P, blockIdx.x);
+struct CodesSmem {
+  float2 qp[16];
+  float qs[16];
+};
+
+// CTA-wide: codes of one chunk (tables and labels read with L2 loads, see
+// label_chunk)
+__device__ __forceinline__ void codes_chunk(const float* __restrict__ x, const QPlan& P,
+                                            const ChunkRef& r, const bsnp_cluster_table* tables,
+                                            const uint8_t* labels, uint8_t* codes,
+                                            CodesSmem& cs, uint64_t pol) {
+  float2* qp = cs.qp;
+  float* qs = cs.qs;
   const int tid = threadIdx.x;
   const bsnp_cluster_table& tb = tables[r.u];
   if (tid < 16) {
-    const float S_ = tb.scales[tid];
+    const float S_ = __ldcg(tb.scales + tid);
     float rc = 0.0f;
     if (S_ > 0.0f) {
       rc = __fdiv_rn(255.0f, S_);
       if (!isfinite(rc)) rc = __int_as_float(0x7fffffff);
     }
-    qp[tid] = make_float2(tb.offsets[tid], rc);
+    qp[tid] = make_float2(__ldcg(tb.offsets + tid), rc);
     qs[tid] = S_;
   }
   __syncthreads();
@@ -390,8 +452,8 @@ __global__ void __launch_bounds__(kQThreads)
     for (int b = 0; b < kB; ++b) {
       const uint32_t i = i0 + b * kQThreads;
       if (i < nv) {
-        v4[b] = ld_stream_f4(src + 4 * i);
-        lw[b] = __ldg(reinterpret_cast<const uint16_t*>(lab) + i);
+        v4[b] = ld_hint_f4(src + 4 * i, pol);
+        lw[b] = __ldcg(reinterpret_cast<const unsigned short*>(lab) + i);
       }
     }
 #pragma unroll
@@ -424,7 +486,7 @@ __global__ void __launch_bounds__(kQThreads)
     }
   }
   for (uint32_t p = 2 * nv + tid; 2 * p < size; p += kQThreads) {
-    const uint32_t byte = lab[p];
+    const uint32_t byte = __ldcg(lab + p);
     for (uint32_t q = 0; q < 2 && 2 * p + q < size; ++q) {
       const float v = src[2 * p + q];
       const uint32_t c = (byte >> (4 * q)) & 15u;
@@ -434,4 +496,12 @@ __global__ void __launch_bounds__(kQThreads)
       cdst[2 * p + q] = (uint8_t)code;
     }
   }
+}
+
+__global__ void __launch_bounds__(kQThreads)
+    quantize_codes_kernel(const float* __restrict__ x, QPlan P,
+                          const bsnp_cluster_table* __restrict__ tables,
+                          const uint8_t* __restrict__ labels, uint8_t* __restrict__ codes) {
+  __shared__ CodesSmem cs;
+  codes_chunk(x, P, chunk_of(P, blockIdx.x), tables, labels, codes, cs, policy_evict_first());
 }

@@ -324,3 +324,27 @@ def test_resident_kernel_repeatable_and_nonfinite(dev):
     x[block * 3 + 5] = float("nan")
     with pytest.raises(Q.QuantizerError, match="non-finite"):
         Q.cluster_encode_device(x, 16, block)
+
+
+@pytest.mark.parametrize("log2b,units,tail", [(13, 9, 0), (13, 8, 100), (16, 8, 1000),
+                                               (17, 10, 8), (20, 8, 0)])
+@pytest.mark.parametrize("dist", ["adam_m", "adam_v", "discrete", "sparse", "offset",
+                                  "uniform"])
+@pytest.mark.parametrize("m", [16, 7, 2])
+def test_many_units_vs_oracle(dev, log2b, units, tail, dist, m):
+    """Encodes of 8-10 units plus a ragged tail: one-sided data (adam_v: the
+    lower fit thresholds lie below every element, so those clusters are
+    empty and decided from the unit extremes), constant blocks (decided
+    directly), discrete / sparse data (the exact min/max round).  Bit-exact
+    vs the oracle."""
+    if log2b == 20 and (m != 16 or dist not in ("adam_m", "discrete")):
+        pytest.skip("size budget")
+    from paper_2511_12376_b200 import quantizer as Q
+    block = 1 << log2b
+    n = units * block + tail
+    rng = np.random.default_rng(log2b * 1000 + m + units)
+    x = _dist(dist, n, rng).astype(np.float32)
+    if dist == "offset":
+        x[2 * block:3 * block] = -0.75    # a constant block (sd = 0)
+    dq = Q.cluster_encode_device(_f32(x, dev), m, block)
+    _check_units(x, m, block, dq)
