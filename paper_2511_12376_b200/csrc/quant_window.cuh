@@ -213,6 +213,51 @@ __device__ __forceinline__ void w_candidates(WSmem& S, float v, uint32_t c, int 
   }
 }
 
+// labels of 4 consecutive elements (nibbles of the returned u16) + their
+// threshold-window candidates and extremes.  LUT path: the 4 LUT bytes are
+// merged into one word (label in the low nibble, flags in bits 6-7 of each
+// byte), so the common case is one test and a nibble pack.
+template <bool kCmp>
+__device__ __forceinline__ uint32_t w_label4(WSmem& S, const float (&v)[4], float gi, float c0,
+                                             int m, float& vmin, float& vmax) {
+  vmin = fmin3(vmin, fminf(v[0], v[1]), fminf(v[2], v[3]));
+  vmax = fmax3(vmax, fmaxf(v[0], v[1]), fmaxf(v[2], v[3]));
+  if (kCmp) {  // two quantize boundaries share a bin: binary search
+    uint32_t c[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      c[q] = count_below(S.B32, v[q]);
+      if ((S.lut[w_bin(v[q], gi, c0)] & kLutN) && w_near(S, v[q], c[q]))
+        w_candidates(S, v[q], c[q], m);
+    }
+    return c[0] | (c[1] << 4) | (c[2] << 8) | (c[3] << 12);
+  }
+  const uint32_t e0 = S.lut[w_bin(v[0], gi, c0)], e1 = S.lut[w_bin(v[1], gi, c0)];
+  const uint32_t e2 = S.lut[w_bin(v[2], gi, c0)], e3 = S.lut[w_bin(v[3], gi, c0)];
+  uint32_t le = __byte_perm(__byte_perm(e0, e1, 0x0040), __byte_perm(e2, e3, 0x0040), 0x5410);
+  uint32_t spec = le & 0xc0c0c0c0u;
+  if (__builtin_expect(spec != 0, 0)) {
+    // rare (~0.3 % of elements): a quantize boundary inside the bin, or a
+    // fit threshold near; each lane walks only its own flagged bytes
+    do {
+      const int q = (__ffs(spec) - 1) >> 3;
+      spec &= ~(0xffu << (8 * q));
+      const uint32_t leq = (le >> (8 * q)) & 0xffu;
+      const float vq = q == 0 ? v[0] : q == 1 ? v[1] : q == 2 ? v[2] : v[3];
+      uint32_t cq = leq & 15u;
+      if ((leq & kLutB) && vq > S.B32[cq]) {
+        ++cq;
+        le += 1u << (8 * q);  // the label nibble stays below 16 (cq < m - 1)
+      }
+      if ((leq & kLutN) && w_near(S, vq, cq)) w_candidates(S, vq, cq, m);
+    } while (spec);
+  }
+  // nibble-pack the 4 labels: c0 | c1 << 4 | c2 << 8 | c3 << 12
+  uint32_t x = le & 0x0f0f0f0fu;
+  x = (x | (x >> 4)) & 0x00ff00ffu;
+  return (x | (x >> 8)) & 0xffffu;
+}
+
 template <bool kCmp>
 __device__ __forceinline__ void w_label_loop(WSmem& S, const float* src, uint32_t size,
                                              uint8_t* lab, int m, float& vmin, float& vmax,
@@ -220,6 +265,7 @@ __device__ __forceinline__ void w_label_loop(WSmem& S, const float* src, uint32_
   const int tid = threadIdx.x;
   const bool vec = ((((uintptr_t)src) & 15) | (((uintptr_t)lab) & 1)) == 0;
   const uint32_t nv = vec ? size / 4 : 0;
+  const float gi = S.gi, c0 = S.c0;
   constexpr int kB = 4;  // vectors per thread in flight
   for (uint32_t i0 = tid; i0 < nv; i0 += kB * kQThreads) {
     float4 v4[kB];
@@ -233,36 +279,8 @@ __device__ __forceinline__ void w_label_loop(WSmem& S, const float* src, uint32_
       const uint32_t i = i0 + b * kQThreads;
       if (i >= nv) break;
       const float v[4] = {v4[b].x, v4[b].y, v4[b].z, v4[b].w};
-      uint32_t le[4], c[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        le[q] = S.lut[w_bin(v[q], S.gi, S.c0)];
-        c[q] = kCmp ? count_below(S.B32, v[q]) : (le[q] & 15u);
-      }
-      vmin = fmin3(vmin, fminf(v[0], v[1]), fminf(v[2], v[3]));
-      vmax = fmax3(vmax, fmaxf(v[0], v[1]), fmaxf(v[2], v[3]));
-      // rare (~0.3 % of elements): a quantize boundary inside the bin, or a
-      // fit threshold near; each lane walks only its own flagged slots
-      uint32_t spec = 0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) spec |= (le[q] & (kLutB | kLutN)) ? (1u << q) : 0u;
-      if (__builtin_expect(spec != 0, 0)) {
-        auto fix = [&](float vq, uint32_t leq, uint32_t& cq) {
-          if (!kCmp && (leq & kLutB)) cq += vq > S.B32[cq] ? 1u : 0u;
-          if ((leq & kLutN) && w_near(S, vq, cq)) w_candidates(S, vq, cq, m);
-        };
-        do {
-          const int q = __ffs(spec) - 1;
-          spec &= spec - 1;
-          if (q == 0) fix(v[0], le[0], c[0]);
-          else if (q == 1) fix(v[1], le[1], c[1]);
-          else if (q == 2) fix(v[2], le[2], c[2]);
-          else fix(v[3], le[3], c[3]);
-        } while (spec);
-      }
-      if (lab)
-        *reinterpret_cast<uint16_t*>(lab + 2 * i) =
-            (uint16_t)(c[0] | (c[1] << 4) | (c[2] << 8) | (c[3] << 12));
+      const uint32_t w = w_label4<kCmp>(S, v, gi, c0, m, vmin, vmax);
+      if (lab) *reinterpret_cast<uint16_t*>(lab + 2 * i) = (uint16_t)w;
     }
   }
   // tail (and unaligned tiles): element pairs (one label byte each)
