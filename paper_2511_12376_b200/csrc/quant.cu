@@ -469,6 +469,7 @@ __global__ void __launch_bounds__(kQThreads)
   const uint64_t full_tiles = (uint64_t)(P.nunits - 1) * P.T_full;
   // grid-stride over tiles: with `need`, only the units the threshold-window
   // pass left undecided are visited (a small grid skips the rest quickly)
+  if (need && !need[P.nunits]) return;  // no unit needs the exact round
   for (uint64_t tile = blockIdx.x; tile < P.total_tiles; tile += gridDim.x) {
     if (need) {
       const uint32_t uu = tile < full_tiles ? (uint32_t)(tile >> P.D_full) : P.nunits - 1;
@@ -507,7 +508,7 @@ __global__ void __launch_bounds__(kQThreads)
                         const uint32_t* __restrict__ need = nullptr) {
   __shared__ int rmin[8][16], rmax[8][16];
   const uint32_t u = blockIdx.x;
-  if (need && !need[u]) return;
+  if (need && (!need[P.nunits] || !need[u])) return;
   uint32_t T;
   uint64_t len;
   unit_shape(P, u, T, len);
@@ -824,7 +825,7 @@ struct QWs {
   int* tile_mm;      // total_tiles * 32
   double* sd;        // nunits
   UGrid* ug;         // nunits
-  uint32_t* need;    // nunits: exact min/max round needed
+  uint32_t* need;    // nunits + 1: exact min/max round needed (per unit, any)
   size_t bytes;
 };
 
@@ -843,7 +844,7 @@ QWs carve(const QPlan& P, void* ws) {
   w.tile_mm = (int*)take(128 * P.total_tiles);
   w.sd = (double*)take(8 * (size_t)P.nunits);
   w.ug = (UGrid*)take(kUGridBytes * (size_t)P.nunits);
-  w.need = (uint32_t*)take(4 * (size_t)P.nunits);
+  w.need = (uint32_t*)take(4 * ((size_t)P.nunits + 1));
   w.bytes = o;
   return w;
 }
@@ -890,7 +891,7 @@ int run_window(const float* x, const QPlan& P, bsnp_cluster_table* tables, uint8
   fit_combine_kernel<true><<<P.nunits, kQThreads, 0, s>>>(P, w.partials, w.mu, w.fthr, tables,
                                                            w.sd);
   if ((rc = launch_status("fit_combine_kernel<std>"))) return rc;
-  fit_grid_kernel<<<P.nunits, kQThreads, 0, s>>>(P, w.mu, w.sd, w.ug);
+  fit_grid_kernel<<<P.nunits, kQThreads, 0, s>>>(P, w.mu, w.sd, w.ug, w.need + P.nunits);
   if ((rc = launch_status("fit_grid_kernel"))) return rc;
   const unsigned chunks = (unsigned)((uint64_t)(P.nunits - 1) * P.C_full + P.C_last);
   fit_label_kernel<<<chunks, kQThreads, 0, s>>>(x, P, w.ug, labels);

@@ -138,10 +138,13 @@ __device__ __forceinline__ void grid_unit(const QPlan& P, uint32_t u, double m0,
     reinterpret_cast<uint4*>(G.lut)[i] = reinterpret_cast<const uint4*>(lut)[i];
 }
 
+// any_need (optional): the "some unit needs the exact round" word, cleared
+// here for fit_decide_kernel to set
 __global__ void __launch_bounds__(kQThreads)
     fit_grid_kernel(QPlan P, const double* __restrict__ mu, const double* __restrict__ sdv,
-                    UGrid* __restrict__ ug) {
+                    UGrid* __restrict__ ug, uint32_t* __restrict__ any_need = nullptr) {
   __shared__ GridSmem g;
+  if (any_need && blockIdx.x == 0 && threadIdx.x == 0) *any_need = 0;
   grid_unit(P, blockIdx.x, mu[blockIdx.x], sdv[blockIdx.x], ug, g);
 }
 
@@ -399,7 +402,10 @@ __device__ __forceinline__ bool decide_unit(const QPlan& P, uint32_t u, const UG
   ok = __all_sync(kFull, ok);
   const uint32_t sk_prev = __shfl_up_sync(kFull, sk, 1);
   const float f_prev = __shfl_up_sync(kFull, f, 1);
-  if (lane == 0) need[u] = ok ? 0u : 1u;
+  if (lane == 0) {
+    need[u] = ok ? 0u : 1u;
+    if (!ok) atomicOr(need + P.nunits, 1u);  // need[nunits]: any unit
+  }
   if (!ok || lane >= 16) return ok;
   const int c = lane;
   float scale = 0.0f, offset = 0.0f;
