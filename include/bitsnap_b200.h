@@ -57,6 +57,13 @@ int bsnp_abi_version(void);
 const char* bsnp_last_error(void);
 /* Number of SMs of the current device (0 if none). */
 int bsnp_device_sm_count(void);
+/* Page-lock / release an existing host range for DMA (cudaHostRegister):
+ * the staging slot region's mapping (replaces the host memcpy of
+ * reference engine.py:225-227 SlotRegion.stage).  A range that cannot be
+ * registered (disk-backed mapping) returns BSNP_E_CUDA and leaves no pending
+ * CUDA error. */
+int bsnp_host_register(void* ptr, size_t bytes);
+int bsnp_host_unregister(void* ptr);
 
 /* ------------------------------------------------------------------------
  * Bitmask delta codec

@@ -24,6 +24,8 @@ SIGNATURES = {
     "bsnp_abi_version": (_i32, []),
     "bsnp_last_error": (_c.c_char_p, []),
     "bsnp_device_sm_count": (_i32, []),
+    "bsnp_host_register": (_i32, [_vp, _sz]),
+    "bsnp_host_unregister": (_i32, [_vp]),
     "bsnp_delta_encode_ws_bytes": (_sz, [_u64]),
     "bsnp_delta_decode_ws_bytes": (_sz, [_u64]),
     "bsnp_delta_encode": (_i32, [_vp, _vp, _u64, _vp, _vp, _u64, _vp, _vp, _sz, _vp]),

@@ -28,3 +28,28 @@ extern "C" int bsnp_device_sm_count(void) {
   }
   return sms;
 }
+
+// Page-lock an existing host range (e.g. a mapped staging region) for DMA.
+// A failed registration (a disk-backed mapping) is cleared from this
+// runtime's error state and reported as BSNP_E_CUDA.
+extern "C" int bsnp_host_register(void* ptr, size_t bytes) {
+  if (!ptr || !bytes) return BSNP_E_INVALID;
+  const cudaError_t e = cudaHostRegister(ptr, bytes, cudaHostRegisterDefault);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    bsnp::set_last_error("cudaHostRegister", e);
+    return BSNP_E_CUDA;
+  }
+  return BSNP_OK;
+}
+
+extern "C" int bsnp_host_unregister(void* ptr) {
+  if (!ptr) return BSNP_E_INVALID;
+  const cudaError_t e = cudaHostUnregister(ptr);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    bsnp::set_last_error("cudaHostUnregister", e);
+    return BSNP_E_CUDA;
+  }
+  return BSNP_OK;
+}

@@ -369,23 +369,30 @@ class CheckpointEncoder:
         returned) — page-locking a fresh multi-GB buffer per save costs
         seconds, so a training loop passes its own (e.g. two alternating
         buffers); a new one is allocated when it is missing or too small."""
+        def dest(manifest, nbytes):
+            if out is not None and out.is_pinned() and out.numel() >= nbytes:
+                return out.reshape(-1).view(torch.uint8)[:nbytes]
+            return torch.empty(max(nbytes, 1), dtype=torch.uint8, pin_memory=True)[:nbytes]
+        return self.encode_into(ckpt, prev, kind, dest)
+
+    def encode_into(self, ckpt: Checkpoint, prev: Checkpoint | None, kind: str, dest):
+        """encode() with the landing zone chosen once the sizes are known:
+        `dest(manifest, nbytes)` returns a host uint8 tensor of nbytes (pinned
+        or registered memory for asynchronous copies) that receives
+        tensors.bin.  Returns (manifest, that tensor)."""
         prev_map = self._prev_map(ckpt, prev, kind)
         items = [(i, GROUP_MODEL, t) for i, t in enumerate(ckpt.model_states)]
         k = len(items)
         items += [(k + i, GROUP_OPTIMIZER, t) for i, t in enumerate(ckpt.optimizer_states)]
         recs, model_dev = self.encode_records(items, prev_map, kind)
         offsets = sequential_offsets(recs)
-        if out is not None and out.is_pinned() and out.numel() >= offsets[-1]:
-            out = out.reshape(-1).view(torch.uint8)[:offsets[-1]]
-        else:
-            out = torch.empty(max(offsets[-1], 1), dtype=torch.uint8,
-                              pin_memory=True)[:offsets[-1]]
-        place_records(recs, offsets, out, self.dev)
         base_iter = ckpt.iteration if kind == KIND_BASE else prev_iteration(prev, self.prev)
         manifest = CheckpointManifest(
             iteration=ckpt.iteration, kind=kind, base_iteration=base_iter,
             tensors=tuple(ManifestEntry(r.name, r.group, r.codec, o, r.length)
                           for r, o in zip(recs, offsets)))
+        out = dest(manifest, offsets[-1])
+        place_records(recs, offsets, out, self.dev)
         if self.keep_prev:
             # the device copies of host inputs become the next delta base;
             # device-resident inputs are referenced (the caller owns them and
@@ -470,6 +477,40 @@ def encode_checkpoint(ckpt: Checkpoint, prev: Checkpoint | None, kind: str,
 # ---------------------------------------------------------------------------
 # load side: chain replay (store.py:418-474) over in-memory blobs
 # ---------------------------------------------------------------------------
+
+BLOB_MAGIC = b"BSBL"
+BLOB_VERSION = 1
+BLOB_HEADER = struct.Struct("<4sHQQQ")  # magic, version, iteration, manifest len, tensors len
+
+
+def blob_header(manifest: CheckpointManifest, mbytes: bytes, tensors_len: int) -> bytes:
+    """The 30-byte head of store.py:275-286's staging blob."""
+    return BLOB_HEADER.pack(BLOB_MAGIC, BLOB_VERSION, manifest.iteration, len(mbytes),
+                            tensors_len)
+
+
+def pack_blob(manifest: CheckpointManifest, tensors) -> bytes:
+    """store.py:275-286: self-contained staging payload (what the async agent
+    persists): header, manifest JSON, tensors.bin."""
+    mbytes = manifest.to_bytes()
+    tb = bytes(tensors.numpy()) if isinstance(tensors, torch.Tensor) else bytes(tensors)
+    return blob_header(manifest, mbytes, len(tb)) + mbytes + tb
+
+
+def unpack_blob(blob) -> tuple:
+    """store.py:289-299 -> (CheckpointManifest, tensors memoryview)."""
+    mv = memoryview(blob)
+    if bytes(mv[:4]) != BLOB_MAGIC:
+        raise StoreError(f"bad blob magic {bytes(mv[:4])!r}")
+    (version,) = struct.unpack_from("<H", mv, 4)
+    if version != BLOB_VERSION:
+        raise StoreError(f"unsupported blob version {version}")
+    _, mlen, tlen = struct.unpack_from("<QQQ", mv, 6)
+    body = mv[BLOB_HEADER.size:]
+    if len(body) != mlen + tlen:
+        raise StoreError("truncated staging blob")
+    return CheckpointManifest.from_bytes(body[:mlen]), body[mlen:mlen + tlen]
+
 
 def _parse_raw(blob: memoryview, off: int):
     cur = ByteCursor(blob[off:])

@@ -1,0 +1,229 @@
+"""Staging slot region and recovery consensus
+against the reference's own engine, run here by
+tests/golden/make_engine_golden.py: the same scripted SlotRegion calls must
+give the same outcomes, slot table, status report and region file bytes;
+the staging blob of the golden checkpoint must give the same file; the
+recovery decisions (consensus and cold start) must match, and the
+torch.distributed consensus (gloo, world 2) must agree with them.  GPU: the
+device hand-off (encoder output DMA'd into the mapped slot) must write the
+same file as staging the reference's blob."""
+
+import hashlib
+import json
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2511_12376_b200 import engine as E
+from paper_2511_12376_b200 import store as S
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+@pytest.fixture(scope="module")
+def eg():
+    with open(os.path.join(GOLDEN, "engine_golden.json")) as f:
+        return json.load(f)
+
+
+def run_script(region, script):
+    out = []
+    for op, *a in script:
+        try:
+            if op == "stage":
+                s = region.stage(a[0], bytes.fromhex(a[1]), a[2])
+                out.append(["ok", s.rank, s.index, s.state, s.iteration, s.length,
+                            str(s.checksum)])
+            elif op == "set_state":
+                region.set_state(*a)
+                out.append(["ok"])
+            elif op == "clear":
+                region.clear_slot(*a)
+                out.append(["ok"])
+            elif op == "verify":
+                out.append(["ok", bool(region.verify(*a))])
+        except E.EngineError as exc:
+            out.append(["raise", type(exc).__name__])
+    return out
+
+
+def test_slot_region_script_matches_reference(eg, tmp_path):
+    path = tmp_path / "script.bssl"
+    region = E.SlotRegion.create(path, **eg["region"])
+    got = run_script(region, eg["script"])
+    want = eg["script_out"]
+    assert got == want["results"]
+    assert [[s.rank, s.index, s.state, s.iteration, s.length, str(s.checksum)]
+            for s in region.all_slots()] == want["slots"]
+    assert E.status_report(region).split("\n")[1:] == want["status"]
+    region.close()
+    assert path.read_bytes().hex() == want["file_hex"]
+    # reopen: header parsed back
+    with E.SlotRegion.open(path) as r2:
+        assert (r2.ranks, r2.redundancy, r2.capacity) == (2, 2, 48)
+        assert r2.verify(0, 0) and r2.payload(0, 0) == b"third"
+
+
+def test_region_checks(eg, tmp_path):
+    assert str(E.EMPTY_CHECKSUM) == eg["empty_checksum"]
+    with pytest.raises(E.EngineError, match=">= 1"):
+        E.SlotRegion.create(tmp_path / "a", 0, 1, 1)
+    bad = tmp_path / "bad"
+    bad.write_bytes(b"XXXX" + bytes(40))
+    with pytest.raises(E.EngineError, match="magic"):
+        E.SlotRegion.open(bad)
+    ver = tmp_path / "ver"
+    ver.write_bytes(E.REGION_HEADER.pack(b"BSSL", 9, 1, 1, 4) + bytes(64))
+    with pytest.raises(E.EngineError, match="version"):
+        E.SlotRegion.open(ver)
+
+
+def test_staging_blob_matches_reference(eg, checkpoint_golden, tmp_path):
+    g = checkpoint_golden
+    man = S.CheckpointManifest.from_bytes(g["manifest1"].tobytes())
+    blob = S.pack_blob(man, g["blob1"].tobytes())
+    cs = eg["checkpoint_stage"]
+    assert len(blob) == cs["blob_len"]
+    m2, t2 = S.unpack_blob(blob)
+    assert m2 == man and bytes(t2) == g["blob1"].tobytes()
+    path = tmp_path / "ckpt.bssl"
+    with E.SlotRegion.create(path, 1, 2, cs["capacity"]) as region:
+        s = region.stage(0, blob, man.iteration)
+        assert str(s.checksum) == cs["checksum"]
+    assert hashlib.sha256(path.read_bytes()).hexdigest() == cs["file_sha256"]
+    with pytest.raises(S.StoreError, match="truncated"):
+        S.unpack_blob(blob[:-1])
+    with pytest.raises(S.StoreError, match="magic"):
+        S.unpack_blob(b"NOPE" + blob[4:])
+
+
+def _consensus_region(path):
+    region = E.SlotRegion.create(path, ranks=2, redundancy=3, capacity=16)
+    region.stage(0, b"r0-it3", 3)
+    region.stage(0, b"r0-it4", 4)
+    region.stage(1, b"r1-it3", 3)
+    s = region.stage(1, b"r1-it4", 4)
+    off = region._slot_offset(1, s.index) + E.SLOT_HEADER.size
+    region._mm[off] ^= 0xFF          # a corrupt copy: fails verify
+    return region
+
+
+def test_recovery_decision_matches_reference(eg, tmp_path):
+    want = eg["recovery"]["consensus"]
+    region = _consensus_region(tmp_path / "r1.bssl")
+    per_rank = [E.region_valid_iterations(region, r) for r in range(region.ranks)]
+    d = E.decide(per_rank)
+    # the reference's single-process recover prunes every rank's slots
+    for r in range(region.ranks):
+        for s in region.slots(r):
+            if s.state != E.STATE_EMPTY and s.iteration > d.chosen_iteration:
+                region.clear_slot(r, s.index)
+                d.pruned.append((r, s.iteration))
+    for r, it in sorted(set(d.pruned)):
+        d.trace.append(f"pruned iteration {it} on rank {r}")
+    d.trace.append(f"recovering from iteration {d.chosen_iteration}")
+    assert d.chosen_iteration == want["chosen"]
+    assert [list(p) for p in sorted(set(d.pruned))] == want["pruned"]
+    assert d.trace == want["trace"]
+    assert [[x.rank, x.index, x.state, x.iteration] for x in region.all_slots()] == want["slots"]
+    region.close()
+    cold = eg["recovery"]["cold"]
+    with pytest.raises(E.ColdStartError, match=cold["message"]):
+        E.decide([{5}, {6}])
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _recover_worker(rank, world, port, path, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        region = E.SlotRegion.open(path)
+        d = E.recover(region, rank)
+        q.put((rank, d.chosen_iteration, d.pruned, d.trace,
+               [[x.index, x.state, x.iteration] for x in region.slots(rank)]))
+        region.close()
+        try:
+            E.decide(E.gather_valid({10 + rank}))
+            q.put((rank, "no-raise"))
+        except E.ColdStartError:
+            q.put((rank, "cold"))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_recover_over_torch_distributed(eg, tmp_path):
+    """Two ranks (gloo) share the region file; each gathers the valid sets,
+    agrees on iteration 3 and clears its own newer slot."""
+    want = eg["recovery"]["consensus"]
+    path = str(tmp_path / "shared.bssl")
+    _consensus_region(path).close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_recover_worker, args=(r, 2, port, path, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(4)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    dec = {r[0]: r for r in res if len(r) == 5}
+    cold = {r[0]: r[1] for r in res if len(r) == 2}
+    assert cold == {0: "cold", 1: "cold"}
+    for rank in (0, 1):
+        _, chosen, pruned, trace, slots = dec[rank]
+        assert chosen == want["chosen"]
+        assert pruned == [(rank, 4)]
+        assert trace[:2] == want["trace"][:2]
+        assert trace[-1] == want["trace"][-1]
+        assert f"pruned iteration 4 on rank {rank}" in trace
+    with E.SlotRegion.open(path) as region:
+        assert [[x.rank, x.index, x.state, x.iteration] for x in region.all_slots()] == \
+            want["slots"]
+
+
+@pytest.mark.gpu
+def test_device_stage_checkpoint_matches_reference(eg, dev, checkpoint_golden, golden_index,
+                                                   tmp_path):
+    """The encoder's records DMA'd into the page-locked slot: the region
+    file equals the one the reference writes when staging its own blob."""
+    from test_store_gpu import _golden_ckpts
+    g, meta = checkpoint_golden, golden_index["checkpoint"]
+    c0, c1 = _golden_ckpts(g, meta)
+    cs = eg["checkpoint_stage"]
+    # tmpfs mappings can be page-locked (DMA); a disk-backed one cannot, and
+    # the copies then go through the driver's staging (same bytes)
+    shm = os.path.isdir("/dev/shm")
+    path = (tmp_path if not shm else
+            __import__("pathlib").Path(tempfile.mkdtemp(dir="/dev/shm"))) / "ckpt.bssl"
+    enc = S.CheckpointEncoder(dev, clusters=16)
+    enc.encode(c0, None, S.KIND_BASE)              # c0 stays resident as the delta base
+    with E.SlotRegion.create(path, 1, 2, cs["capacity"]) as region:
+        if shm:
+            assert region.dma_ready
+        info, man = region.stage_checkpoint(0, enc, c1, None, S.KIND_DELTA)
+        assert info.state == E.STATE_VALID and info.length == cs["blob_len"]
+        assert str(info.checksum) == cs["checksum"] and region.verify(0, info.index)
+        m2, tb = S.unpack_blob(region.payload(0, info.index))
+        assert m2.to_bytes() == g["manifest1"].tobytes() and bytes(tb) == g["blob1"].tobytes()
+        with pytest.raises(E.StaleIterationError):
+            region.stage_checkpoint(0, enc, c1, c0, S.KIND_DELTA)
+    assert hashlib.sha256(path.read_bytes()).hexdigest() == cs["file_sha256"]
+    path.unlink()
+    if shm:
+        path.parent.rmdir()
+    # a disk-backed region: no page-locking, same bytes
+    with E.SlotRegion.create(tmp_path / "disk.bssl", 1, 2, cs["capacity"]) as region:
+        info, _ = region.stage_checkpoint(0, enc, c1, c0, S.KIND_DELTA)
+        m2, tb = S.unpack_blob(region.payload(0, info.index))
+        assert bytes(tb) == g["blob1"].tobytes()
