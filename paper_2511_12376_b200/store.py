@@ -544,21 +544,32 @@ def _parse_delta(blob: memoryview, off: int):
     return name, shape, n, n_c, mo, po
 
 
-def decode_chain(chain, device: torch.device | None = None, to_host: bool = True):
+def decode_chain(chain, device: torch.device | None = None, to_host: bool = True,
+                 base: Checkpoint | None = None):
     """Reconstruct the last checkpoint of `chain` = [(manifest, tensors_blob)]
     (blob: bytes-like, or a pinned uint8 tensor used in place)
     in ascending iteration order, the first being a base (store.py:429-474
     after the manifests were read).  Model states are rebuilt on the device by
     in-place delta application; optimizer states of the final manifest are
-    dequantized.  Returns a reference `Checkpoint` of TensorBlobs, or of
-    DeviceTensors with `to_host=False`."""
+    dequantized.  With `base` (a decoded checkpoint: TensorBlobs or
+    DeviceTensors) the chain may start with a delta against its model states
+    (metrics.py:169-192's in-memory decode).  Returns a reference
+    `Checkpoint` of TensorBlobs, or of DeviceTensors with `to_host=False`."""
     dev = rt.device_of() if device is None else torch.device(device)
-    if not chain or chain[0][0].kind != KIND_BASE:
+    if not chain or (base is None and chain[0][0].kind != KIND_BASE):
         raise StoreError("chain must start with a base checkpoint")
     model: dict = {}
     meta: dict = {}
     model_order: list = []
     final_opt = []
+    if base is not None:
+        up = _Uploader(dev, [t for t in base.model_states if not isinstance(t, DeviceTensor)])
+        for t in base.model_states:  # copies: deltas apply in place
+            flat = _device_flat(t, up).reshape(-1).clone()
+            model[t.name] = flat.view(torch.int16 if t.dtype is ElementType.F16
+                                      else torch.float32)
+            meta[t.name] = (t.dtype, tuple(t.shape))
+            model_order.append(t.name)
     with torch.cuda.device(dev):
         for ci, (manifest, blob) in enumerate(chain):
             if isinstance(blob, torch.Tensor) and blob.is_pinned():
