@@ -776,7 +776,6 @@ __global__ void __launch_bounds__(kQThreads)
   }
 }
 
-#include "quant_resident.cuh"
 #include "quant_window.cuh"
 
 // ---------------------------------------------------------------- host plan
@@ -918,45 +917,19 @@ using namespace bsnp;
 extern "C" size_t bsnp_cluster_ws_bytes(uint64_t n, uint64_t block) {
   QPlan P;
   if (!make_plan(n ? n : 1, block, 16, P)) return 0;
-  size_t b = carve(P, nullptr).bytes;
-  const uint64_t ru = resident_units(n, block);
-  if (ru) b = std::max(b, resident_ws_bytes(ru, (uint32_t)(block / kRTile)));
-  return b;
+  return carve(P, nullptr).bytes;
 }
 
-// Per-block calls: full power-of-two blocks may take the resident-tile kernel
-// (opt-in); everything else, and the tail, the tiled window kernels.
 static int cluster_run(const float* x, uint64_t n, uint64_t block, int m,
                        bsnp_cluster_table* tables, uint8_t* labels, uint8_t* codes, void* ws,
                        size_t ws_bytes, cudaStream_t s) {
-  const bool quant = labels != nullptr;
-  const bool aligned = ((((uintptr_t)x) & 15) | (((uintptr_t)codes) & 3) | (((uintptr_t)labels) & 1)) == 0;
-  // full power-of-two blocks: the resident-tile kernel (one HBM read of x)
-  const uint64_t ru = aligned ? resident_units(n, block) : 0;
-  if (ru && ws_bytes >= resident_ws_bytes(ru, (uint32_t)(block / kRTile))) {
-    int rc = launch_resident(x, ru, block, m, tables, labels, codes, quant ? 1 : 0, ws, s);
-    if (rc == BSNP_OK) {
-      const uint64_t done = ru * block;
-      if (done == n) return BSNP_OK;
-      x += done;
-      tables += ru;
-      if (quant) {
-        labels += done / 2;
-        codes += done;
-      }
-      n -= done;
-      block = 0;
-    } else if (rc != BSNP_E_INVALID) {
-      return rc;
-    }
-  }
   QPlan P;
   if (!make_plan(n, block, m, P)) return BSNP_E_INVALID;
   const QWs w = carve(P, ws);
   if (ws_bytes < w.bytes) return BSNP_E_WORKSPACE;
   if (window_enabled()) return run_window(x, P, tables, labels, codes, w, s);
   int rc = run_fit(x, P, tables, w, s);
-  if (rc || !quant) return rc;
+  if (rc || !labels) return rc;
   quantize_kernel<<<(unsigned)P.total_tiles, kQThreads, 0, s>>>(x, P, tables, labels, codes);
   return launch_status("quantize_kernel");
 }

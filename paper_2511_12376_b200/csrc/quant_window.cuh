@@ -1,5 +1,5 @@
-// Tiled cluster encoder, threshold-window variant (included by quant.cu after
-// quant_resident.cuh, inside its anonymous namespace; the default encode path).
+// Tiled cluster encoder, threshold-window variant (included by quant.cu
+// inside its anonymous namespace; the default encode path).
 //
 // The fit's per-cluster min/max pass and the quantize pass of the tiled
 // kernels are replaced by:
@@ -27,6 +27,35 @@
 // delta = 80 sd / n: for dense data pred/succ are ~sd/(n pdf) away (<= 8.3
 // sd / n for every threshold of m <= 16), so a missing side (probability
 // <= e^-9.6 per threshold side) only costs the exact round of that unit.
+// LUT byte: bits 0-3 L = #quantize boundaries in lower bins; bit 7: boundary L
+// lies in this bin (label = L + (v > B32[L])); bit 6: kLutN below.
+constexpr uint32_t kLutB = 0x80u;
+
+// order-preserving float -> u32 (0 is below every non-NaN key)
+__device__ __forceinline__ uint32_t ukey(float f) {
+  const uint32_t b = __float_as_uint(f);
+  return b ^ (uint32_t)(((int)b >> 31) | (int)0x80000000);
+}
+__device__ __forceinline__ float ukey_inv(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k ^ 0x80000000u) : ~k);
+}
+__device__ __forceinline__ float fmin3(float a, float b, float c) {
+  float r;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+// ceil to u8 with saturation (the reference's clip(ceil(..), 0, 255))
+__device__ __forceinline__ uint32_t ceil_u8(float t) {
+  uint32_t r;
+  asm("cvt.rpi.sat.u8.f32 %0, %1;" : "=r"(r) : "f"(t));
+  return r;
+}
+
 constexpr uint32_t kWDeltaNum = 80;
 constexpr int kWBins = 16384;           // label LUT bins over mu +- 2 sd
 constexpr uint32_t kLutN = 0x40u;       // LUT bit: the bin meets some [F_k - delta, F_k + delta]

@@ -290,11 +290,11 @@ def _dist(name, n, rng):
 @pytest.mark.parametrize("dist", ["adam_m", "adam_v", "discrete", "sparse", "offset",
                                   "uniform"])
 @pytest.mark.parametrize("m", [16, 7, 2])
-def test_resident_kernel_vs_oracle(dev, log2b, units, tail, dist, m):
-    """Power-of-two blocks of 2^13..2^21 take the resident-tile kernel (one
-    HBM read) when enabled (BSNP_RESIDENT=1), else the tiled kernels; the
-    tail unit always the tiled kernels.  Sparse/discrete data force its exact
-    min/max round.  Every unit is bit-exact vs the oracle."""
+def test_power_of_two_blocks_vs_oracle(dev, log2b, units, tail, dist, m):
+    """Power-of-two blocks of 2^13..2^21 (perfect tree tiles) plus a ragged
+    tail unit; sparse/discrete data force the exact min/max round.  Every
+    unit is bit-exact vs the oracle, and the fit-only path gives the same
+    tables."""
     if (log2b >= 20 and m != 16) or (log2b == 21 and dist not in ("adam_m", "discrete")):
         pytest.skip("size budget")
     from paper_2511_12376_b200 import quantizer as Q
@@ -310,7 +310,7 @@ def test_resident_kernel_vs_oracle(dev, log2b, units, tail, dist, m):
     assert bytes(tables.cpu().numpy()) == bytes(dq.tables.cpu().numpy())
 
 
-def test_resident_kernel_repeatable_and_nonfinite(dev):
+def test_repeatable_and_nonfinite(dev):
     import torch
     from paper_2511_12376_b200 import quantizer as Q
     n, block = 1 << 22, 1 << 18

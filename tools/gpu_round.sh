@@ -1,12 +1,12 @@
 #!/bin/bash
-# Full GPU check: build, all GPU tests (+ resident/legacy quantizer variants),
+# Full GPU check: build, all GPU tests (+ the four-pass quantizer variant),
 # smoke, bench (b200 + reference arm), ncu launch list of the bench and a
 # full capture of the C1 and C2 top kernels.
 tag=${1:-r}
 cd "${GRAFT_REPO_ROOT:-.}"; mkdir -p gpurun_out
 python -m paper_2511_12376_b200._build > gpurun_out/build_$tag.log 2>&1
 timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu_$tag.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu_$tag.log
-BSNP_RESIDENT=1 timeout 900 python -m pytest tests/test_quantizer_gpu.py -q > gpurun_out/pytest_resident_$tag.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_resident_$tag.log
+BSNP_WINDOW=0 timeout 900 python -m pytest tests/test_quantizer_gpu.py -q > gpurun_out/pytest_minmax_$tag.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_minmax_$tag.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$tag.log 2>&1; echo "rc=$?" >> gpurun_out/smoke_$tag.log
 timeout 900 python bench.py > gpurun_out/bench_$tag.json 2> gpurun_out/bench_$tag.err
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_$tag.json 2> gpurun_out/bench_ref_$tag.err
