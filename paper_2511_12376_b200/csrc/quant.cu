@@ -713,23 +713,38 @@ __global__ void __launch_bounds__(kQThreads)
                     (((uintptr_t)(o + c0)) & 15)) == 0;
   uint64_t e = c0;
   if (vec) {
-    const uint64_t nv = (c1 - c0) / 8;
-    for (uint64_t i = threadIdx.x; i < nv; i += blockDim.x) {
-      const uint64_t e0 = c0 + 8 * i;
-      const uint2 cc = *reinterpret_cast<const uint2*>(cs + e0);
-      const uint32_t ll = *reinterpret_cast<const uint32_t*>(ls + e0 / 2);
-      float r[8];
+    const uint32_t nv = (uint32_t)((c1 - c0) / 8);
+    constexpr int kB = 4;  // 8-element groups per thread with loads in flight
+    for (uint32_t i0 = threadIdx.x; i0 < nv; i0 += kB * kQThreads) {
+      uint2 cc[kB];
+      uint32_t ll[kB];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const uint32_t lab = (ll >> (4 * k)) & 15u;
-        const uint32_t code = ((k < 4 ? cc.x : cc.y) >> (8 * (k & 3))) & 255u;
-        maxlab = lab > maxlab ? lab : maxlab;
-        r[k] = lut[lab * 256 + code];
+      for (int b = 0; b < kB; ++b) {
+        const uint32_t i = i0 + b * kQThreads;
+        if (i < nv) {
+          const uint64_t e0 = c0 + 8ull * i;
+          cc[b] = __ldg(reinterpret_cast<const uint2*>(cs + e0));
+          ll[b] = __ldg(reinterpret_cast<const uint32_t*>(ls + e0 / 2));
+        }
       }
-      *reinterpret_cast<float4*>(o + e0) = make_float4(r[0], r[1], r[2], r[3]);
-      *reinterpret_cast<float4*>(o + e0 + 4) = make_float4(r[4], r[5], r[6], r[7]);
+#pragma unroll
+      for (int b = 0; b < kB; ++b) {
+        const uint32_t i = i0 + b * kQThreads;
+        if (i >= nv) break;
+        const uint64_t e0 = c0 + 8ull * i;
+        float r[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t lab = (ll[b] >> (4 * k)) & 15u;
+          const uint32_t code = ((k < 4 ? cc[b].x : cc[b].y) >> (8 * (k & 3))) & 255u;
+          maxlab = lab > maxlab ? lab : maxlab;
+          r[k] = lut[lab * 256 + code];
+        }
+        *reinterpret_cast<float4*>(o + e0) = make_float4(r[0], r[1], r[2], r[3]);
+        *reinterpret_cast<float4*>(o + e0 + 4) = make_float4(r[4], r[5], r[6], r[7]);
+      }
     }
-    e = c0 + nv * 8;
+    e = c0 + (uint64_t)nv * 8;
   }
   for (uint64_t i = e + threadIdx.x; i < c1; i += blockDim.x) {
     const uint32_t lab = (ls[i / 2] >> (4 * (i & 1))) & 15u;
