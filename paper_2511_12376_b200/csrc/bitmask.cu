@@ -240,7 +240,6 @@ __global__ void __launch_bounds__(kEncThreads)
   __shared__ uint32_t s_tile[kStages];
   __shared__ uint32_t r_tile[kRing], r_count[kRing];
   __shared__ uint64_t s_warp[2][kWarps];
-  __shared__ uint32_t s_off[2][kVec][kWarps];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t nfull = n / kTile;
@@ -380,18 +379,24 @@ __global__ void __launch_bounds__(kEncThreads)
     asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
     // every worker holds its part of the tile in registers: release the stage
     if (tid == 0) refill(s, next_t);
-    if (warp == 0) {
+    // every warp scans the 8 warp totals itself (lane = group j * 8 + warp w,
+    // the tile's element order), so no second barrier waits on warp 0's
+    // publish / record hand-off
+    uint32_t woff[kVec];
+    {
       const int j = lane / kWarps, w = lane % kWarps;
       const uint32_t v = (uint32_t)(s_warp[db][w] >> (16 * j)) & 0xffffu;
       const uint32_t x = warp_inclusive_scan_u32(v, lane);
-      s_off[db][j][w] = x - v;
-      const uint32_t total = __shfl_sync(kFull, x, 31);
-      if (lane == 0) {
-        publish_aggregate(tile_status, tile, total);
-        push_record(q, tile, total);
+#pragma unroll
+      for (int jj = 0; jj < kVec; ++jj) woff[jj] = __shfl_sync(kFull, x - v, jj * kWarps + warp);
+      if (warp == 0) {
+        const uint32_t total = __shfl_sync(kFull, x, 31);
+        if (lane == 0) {
+          publish_aggregate(tile_status, tile, total);
+          push_record(q, tile, total);
+        }
       }
     }
-    asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
     const uint64_t ex = inc - packed;
     const uint64_t g0 = t0 / 8;
 #pragma unroll
@@ -403,7 +408,7 @@ __global__ void __launch_bounds__(kEncThreads)
 #pragma unroll
     for (int j = 0; j < kVec; ++j) {
       uint32_t b = bits[j];
-      uint32_t pos = s_off[db][j][warp] + ((uint32_t)(ex >> (16 * j)) & 0xffffu);
+      uint32_t pos = woff[j] + ((uint32_t)(ex >> (16 * j)) & 0xffffu);
       while (b) {
         const uint32_t k = __ffs(b) - 1;
         b &= b - 1;
