@@ -493,10 +493,15 @@ __global__ void __launch_bounds__(kThreads)
 
 template <int kStages, bool kDense>
 __global__ void __launch_bounds__(kThreads)
-    delta_decode_tma_kernel(const uint16_t* __restrict__ base, const uint8_t* __restrict__ mask,
+    delta_decode_tma_kernel(const uint16_t* base, const uint8_t* __restrict__ mask,
                             const uint16_t* __restrict__ payload, uint64_t n, uint64_t n_c,
-                            uint16_t* __restrict__ out, const uint64_t* __restrict__ offsets,
-                            uint32_t* __restrict__ ticket) {
+                            uint16_t* out, const uint64_t* __restrict__ offsets,
+                            uint32_t* __restrict__ ticket,
+                            const bsnp_status* __restrict__ st) {
+  // in place (out == base, dense chain replay): every tile is read by TMA
+  // into shared memory before its words are written, tiles are disjoint, and
+  // a record the validation pass rejected leaves the base untouched
+  if (st && *(volatile const uint32_t*)&st->err_flags) return;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t full_bar[kStages];
   __shared__ uint32_t s_tile[kStages];
@@ -876,7 +881,14 @@ extern "C" int bsnp_delta_decode(const uint16_t* base, const uint8_t* mask,
   if ((rc = launch_status("delta_offsets_kernel"))) return rc;
   const bool in_place = (const void*)base == (const void*)out;
   const bool aligned = (((uintptr_t)base | (uintptr_t)out | (uintptr_t)mask) & 15) == 0;
-  if (in_place) {
+  if (in_place && aligned && n_c * 32 > n) {
+    // dense: streaming the whole tile beats touching the changed words
+    // (p = 25 %: 0.77 vs 1.27 ms at 2^30)
+    const size_t smem = (size_t)kDecStages * kDecStage;
+    auto k = delta_decode_tma_kernel<kDecStages, true>;
+    const int grid = persistent_grid(k, smem, nt);
+    k<<<grid, kThreads, smem, s>>>(base, mask, payload, n, n_c, out, offsets, ticket2, status);
+  } else if (in_place) {
     static int sms = 0;
     if (!sms) {
       int dev = 0;
@@ -891,7 +903,7 @@ extern "C" int bsnp_delta_decode(const uint16_t* base, const uint8_t* mask,
     auto k = n_c * 32 > n ? delta_decode_tma_kernel<kDecStages, true>
                           : delta_decode_tma_kernel<kDecStages, false>;
     const int grid = persistent_grid(k, smem, nt);
-    k<<<grid, kThreads, smem, s>>>(base, mask, payload, n, n_c, out, offsets, ticket2);
+    k<<<grid, kThreads, smem, s>>>(base, mask, payload, n, n_c, out, offsets, ticket2, nullptr);
   } else {
     delta_apply_kernel<false><<<(unsigned)nt, kThreads, 0, s>>>(base, mask, payload, n, n_c,
                                                                  out, offsets, status);

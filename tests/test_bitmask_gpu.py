@@ -257,3 +257,28 @@ def test_hostpath_roundtrip_matches_oracle(dev):
     rec2 = codec.encode(bh, ch)
     assert np.array_equal(rec2.mask.numpy(), mask)
     assert np.array_equal(codec.decode(bh, rec2).numpy().view(np.uint16), cur)
+
+
+@pytest.mark.parametrize("n,p", [((1 << 20) + 777, 0.25), ((1 << 20) + 3, 0.0625),
+                                 (8192 * 5, 0.5), (100003, 0.04)])
+def test_in_place_apply_dense(dev, n, p):
+    """Chain replay at dense change fractions streams whole tiles in place
+    (decode kernel with out == base) instead of touching changed words; the
+    result equals the target, and a rejected record leaves the base as is."""
+    import torch
+    from paper_2511_12376_b200 import bitmask as B
+    rng = np.random.default_rng(int(n * p))
+    base = rng.integers(0, 1 << 16, n, dtype=np.uint16)
+    cur = base.copy()
+    idx = rng.choice(n, int(n * p), replace=False)
+    cur[idx] ^= rng.integers(1, 1 << 16, idx.size, dtype=np.uint16)
+    d = B.encode_delta_device(_dev_u16(base, dev), _dev_u16(cur, dev))
+    bt = _dev_u16(base, dev)
+    B.decode_delta_device(bt, d.mask, d.payload, d.n_c, out=bt)
+    assert np.array_equal(bt.cpu().numpy().view(np.uint16), cur)
+    bt = _dev_u16(base, dev)
+    bad = d.mask.clone()
+    bad[0] ^= 1                      # popcount no longer matches n_c
+    with pytest.raises(B.DeltaError, match="popcount"):
+        B.decode_delta_device(bt, bad, d.payload, d.n_c, out=bt)
+    assert np.array_equal(bt.cpu().numpy().view(np.uint16), base)
