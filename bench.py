@@ -321,7 +321,8 @@ def run_b200(args, rank: int, world: int, local_rank: int):
                      "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": round(achieved / hbm, 4),
                      "algorithmic_bytes": dom_bytes,
-                     "traffic": traffic},
+                     "traffic": traffic["bytes"] if traffic else None,
+                     "traffic_detail": traffic},
         "gpu_launches": 3 * args.steps,  # encode, offsets, decode per step
         "clocks": clk,
     }
@@ -391,12 +392,16 @@ def run_c2(args, dev, world):
             "roofline_encode": {"bound": "hbm", "achieved": round(enc_gbs / world, 1),
                                 "peak": hbm, "peak_kind": kind, "unit": "GB/s",
                                 "frac": round(enc_gbs / world / hbm, 4),
-                                "algorithmic_bytes": algo, "traffic": traffic},
+                                "algorithmic_bytes": algo,
+                                "traffic": traffic["bytes"] if traffic else None,
+                                "traffic_detail": traffic},
             "roofline_decode": {"bound": "hbm", "achieved": round(dec_gbs / world, 1),
                                 "peak": hbm, "peak_kind": kind, "unit": "GB/s",
                                 "frac": round(dec_gbs / world / hbm, 4),
                                 "algorithmic_bytes": algo,
-                                "traffic": ncu_traffic().get("cluster_dequantize")},
+                                "traffic": (ncu_traffic().get("cluster_dequantize") or {})
+                                .get("bytes"),
+                                "traffic_detail": ncu_traffic().get("cluster_dequantize")},
             "compression_ratio": round(4 * n / enc_bytes, 4),
             "max_abs_err": err}
 
