@@ -159,6 +159,31 @@ int bsnp_cluster_dequantize(const uint8_t* labels, const uint8_t* codes, uint64_
                             uint64_t block, const bsnp_cluster_table* tables, float* out,
                             bsnp_status* status, void* ws, size_t ws_bytes, void* stream);
 
+/* ------------------------------------------------------------------------
+ * Checkpoint blob assembly
+ * ---------------------------------------------------------------------- */
+
+/* len bytes from device address src to blob + dst_off */
+typedef struct bsnp_segment {
+  const void* src;
+  uint64_t dst_off;
+  uint64_t len;
+} bsnp_segment;
+
+/* Chunk size of bsnp_gather_segments (bytes per CTA). */
+#define BSNP_GATHER_CHUNK 65536u
+
+/*
+ * Assembles tensors.bin in device memory: every record's header and bodies
+ * at its store offset (store.py:240-270 writes them one by one into a host
+ * buffer).  segs / first live in device memory; first[s] is the index of
+ * segment s's first BSNP_GATHER_CHUNK chunk and nchunks = first[nsegs] (the
+ * chunk total, passed by value so the launch needs no read-back).  The blob
+ * then leaves HBM in a single device-to-host copy.
+ */
+int bsnp_gather_segments(const bsnp_segment* segs, const uint32_t* first, uint32_t nsegs,
+                         uint32_t nchunks, uint8_t* blob, void* stream);
+
 /*
  * Reduction behind precision_report (quantizer.py:280-296): acc3 receives
  * { sum (o-r)^2, sum |o-r|/|o| over |o| > 1e-12, count of |o| > 1e-12 } in

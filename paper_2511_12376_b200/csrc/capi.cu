@@ -53,3 +53,74 @@ extern "C" int bsnp_host_unregister(void* ptr) {
   }
   return BSNP_OK;
 }
+
+// ---------------------------------------------------------------------------
+// checkpoint blob assembly: one CTA per 64 KiB chunk of a segment
+namespace {
+__global__ void __launch_bounds__(256)
+    gather_segments_kernel(const bsnp_segment* __restrict__ segs,
+                           const uint32_t* __restrict__ first, uint32_t nsegs,
+                           uint8_t* __restrict__ blob) {
+  __shared__ uint32_t s_seg;
+  const uint32_t b = blockIdx.x;
+  if (threadIdx.x == 0) {
+    uint32_t lo = 0, hi = nsegs;  // largest s with first[s] <= b
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (first[mid] <= b) lo = mid;
+      else hi = mid;
+    }
+    s_seg = lo;
+  }
+  __syncthreads();
+  const bsnp_segment sg = segs[s_seg];
+  const uint64_t c0 = (uint64_t)(b - first[s_seg]) * BSNP_GATHER_CHUNK;
+  if (c0 >= sg.len) return;
+  const uint64_t len = sg.len - c0 < BSNP_GATHER_CHUNK ? sg.len - c0 : BSNP_GATHER_CHUNK;
+  const uint8_t* src = static_cast<const uint8_t*>(sg.src) + c0;
+  uint8_t* dst = blob + sg.dst_off + c0;
+  const uint32_t n = (uint32_t)len;
+  const uint32_t mis = (uint32_t)(((uintptr_t)src ^ (uintptr_t)dst) & 15);
+  uint32_t head = 0;
+  if (mis == 0) {
+    head = (uint32_t)((16 - ((uintptr_t)dst & 15)) & 15);
+    if (head > n) head = n;
+    const uint32_t nv = (n - head) / 16;
+    const uint4* s4 = reinterpret_cast<const uint4*>(src + head);
+    uint4* d4 = reinterpret_cast<uint4*>(dst + head);
+    for (uint32_t i = threadIdx.x; i < nv; i += blockDim.x) d4[i] = s4[i];
+    for (uint32_t i = threadIdx.x; i < head; i += blockDim.x) dst[i] = src[i];
+    for (uint32_t i = head + nv * 16 + threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+  } else {
+    // dst-aligned 32-bit words built from two aligned source words with a
+    // funnel shift (the byte offset between source and destination is the
+    // same for the whole segment)
+    head = (uint32_t)((4 - ((uintptr_t)dst & 3)) & 3);
+    if (head > n) head = n;
+    for (uint32_t i = threadIdx.x; i < head; i += blockDim.x) dst[i] = src[i];
+    const uint32_t nw = (n - head) / 4;
+    const uint8_t* s0 = src + head;
+    const uint32_t sh = (uint32_t)((uintptr_t)s0 & 3) * 8;
+    const uint32_t* sw = reinterpret_cast<const uint32_t*>((uintptr_t)s0 & ~(uintptr_t)3);
+    uint32_t* dw = reinterpret_cast<uint32_t*>(dst + head);
+    if (sh == 0) {
+      for (uint32_t i = threadIdx.x; i < nw; i += blockDim.x) dw[i] = sw[i];
+    } else {
+      // the last word pair may read up to 3 bytes past the segment's source
+      // end; those bytes stay inside the 4-byte word holding its last byte
+      for (uint32_t i = threadIdx.x; i < nw; i += blockDim.x)
+        dw[i] = __funnelshift_r(sw[i], sw[i + 1], sh);
+    }
+    for (uint32_t i = head + nw * 4 + threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+  }
+}
+}  // namespace
+
+extern "C" int bsnp_gather_segments(const bsnp_segment* segs, const uint32_t* first,
+                                    uint32_t nsegs, uint32_t nchunks, uint8_t* blob,
+                                    void* stream) {
+  if (nsegs == 0 || nchunks == 0) return BSNP_OK;
+  if (!segs || !first || !blob) return BSNP_E_INVALID;
+  gather_segments_kernel<<<nchunks, 256, 0, (cudaStream_t)stream>>>(segs, first, nsegs, blob);
+  return bsnp::launch_status("gather_segments_kernel");
+}

@@ -230,3 +230,41 @@ def test_planner_two_ranks_one_gpu(dev, tmp_path):
     assert open(path, "rb").read() == want
     assert mans[0] == mans[1]
     assert [vars(e) for e in S.CheckpointManifest.from_bytes(mans[0]).tensors] == entries
+
+
+def test_graph_replay_of_repeated_saves(dev, checkpoint_golden, golden_index):
+    """Device-resident saves of the same tensors: the first runs eagerly, the
+    second records the launch sequence as a CUDA graph, later ones replay it
+    (after the inputs changed in place): every blob equals the reference's."""
+    g, meta = checkpoint_golden, golden_index["checkpoint"]
+    c0, c1 = _golden_ckpts(g, meta)
+
+    def on_device(c):
+        ms = [S.DeviceTensor(t.name, t.dtype, t.shape,
+                             torch.from_numpy(np.frombuffer(t.data, np.int16).copy()).to(dev))
+              for t in c.model_states]
+        os_ = [S.DeviceTensor(t.name, t.dtype, t.shape,
+                              torch.from_numpy(np.frombuffer(t.data, np.float32).copy()).to(dev))
+               for t in c.optimizer_states]
+        return Checkpoint(iteration=c.iteration, model_states=ms, optimizer_states=os_)
+
+    d0, d1 = on_device(c0), on_device(c1)
+    zero = on_device(c0)
+    for t in zero.optimizer_states:
+        t.data.zero_()
+    enc = S.CheckpointEncoder(dev, clusters=16, keep_prev=False)
+    for rep in range(4):
+        if rep == 3:   # same addresses, new contents: the replay must see them
+            for a, b in zip(d1.optimizer_states, zero.optimizer_states):
+                a.data.copy_(b.data)
+        man, out = enc.encode(d1, d0, S.KIND_DELTA)
+        if rep < 3:
+            assert out.numpy().tobytes() == g["blob1"].tobytes(), rep
+            assert man.to_bytes() == g["manifest1"].tobytes()
+        else:
+            ref, _ = S.CheckpointEncoder(dev, clusters=16, keep_prev=False).encode(
+                Checkpoint(iteration=110, model_states=c1.model_states,
+                           optimizer_states=[t.to_blob() for t in zero.optimizer_states]),
+                c0, S.KIND_DELTA)
+            assert man.to_bytes() == ref.to_bytes()
+    assert len(enc._graphs) == 1
