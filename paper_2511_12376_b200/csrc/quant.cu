@@ -671,6 +671,94 @@ __global__ void __launch_bounds__(kQThreads)
   }
 }
 
+// ------------------------------------------------------- one-tile units
+// A unit of at most kTileMax elements (biases, norms: 2/3 of a GPT-2
+// checkpoint's optimizer tensors) in ONE CTA: x stays in shared memory
+// through the pairwise mean and variance trees, the table, the fit-label
+// min/max and the codes - one launch instead of the tiled path's ten.
+// Same primitives, so the same bits.
+__global__ void __launch_bounds__(kQThreads)
+    tiny_encode_kernel(const float* __restrict__ x, uint32_t n, int m,
+                       bsnp_cluster_table* __restrict__ tbl, uint8_t* __restrict__ labels,
+                       uint8_t* __restrict__ codes) {
+  __shared__ __align__(16) float s[kSmemFloats];
+  __shared__ Heap H;
+  __shared__ QuantParams Q;
+  __shared__ float F[16];
+  __shared__ int cmin[16], cmax[16];
+  __shared__ double s_mu, s_sd;
+  const int tid = threadIdx.x;
+  load_tile(s, x, n, policy_evict_first());
+  if (tid < 16) {
+    cmin[tid] = 0x7fffffff;
+    cmax[tid] = (int)0x80000000;
+  }
+  __syncthreads();
+  const double sum = tree_sum<false>(s, n, 0.0, H);
+  if (tid == 0) s_mu = __ddiv_rn(__dadd_rn(0.0, sum), (double)n);  // np.mean
+  __syncthreads();
+  const double mu = s_mu;
+  const double sq = tree_sum<true>(s, n, mu, H);
+  if (tid == 0) s_sd = __dsqrt_rn(__ddiv_rn(__dadd_rn(0.0, sq), (double)n));  // np.std
+  __syncthreads();
+  const double sd = s_sd;
+  if (tid < 16) {
+    float f = __int_as_float(0x7f800000), b32 = f;
+    if (tid < m - 1) {
+      const double b = __dadd_rn(mu, __dmul_rn(sd, kNdtri[m][tid]));
+      f = __double2float_rd(b);   // fit labels compare against b exactly
+      b32 = __double2float_rn(b);
+    }
+    F[tid] = f;
+    Q.bnd[tid] = b32;
+  }
+  __syncthreads();
+  // fit labels (#(B64_k < v) == #(F_k < v)) and per-cluster extremes
+  for (uint32_t i = tid; i < n; i += kQThreads) {
+    const float v = s[padded(i)];
+    const uint32_t c = count_below(F, v);
+    const int k = fkey(v);
+    atomicMin(&cmin[c], k);
+    atomicMax(&cmax[c], k);
+  }
+  __syncthreads();
+  if (tid < 16) {
+    float scale = 0.0f, offset = 0.0f;
+    if (tid < m && cmin[tid] <= cmax[tid]) {
+      const float lo = fkey_inv(cmin[tid]), hi = fkey_inv(cmax[tid]);
+      scale = __double2float_rn(__dsub_rn((double)hi, (double)lo));
+      offset = lo;
+    }
+    Q.off[tid] = offset;
+    Q.scl[tid] = scale;
+    float rc = 0.0f;
+    if (scale > 0.0f) {
+      rc = __fdiv_rn(255.0f, scale);
+      if (!isfinite(rc)) rc = __int_as_float(0x7fffffff);
+    }
+    Q.rcp[tid] = rc;
+    if (tid == 0) Q.last = (uint32_t)m - 1;
+    tbl->scales[tid] = scale;
+    tbl->offsets[tid] = offset;
+    if (tid < 15) tbl->boundaries[tid] = tid < m - 1 ? Q.bnd[tid] : 0.0f;
+    if (tid < 13) tbl->reserved[tid] = 0;
+    if (tid == 0) {
+      tbl->mean = __double2float_rn(mu);
+      tbl->std = __double2float_rn(sd);
+      tbl->m = (uint32_t)m;
+      tbl->flags = (isfinite(mu) && isfinite(sd)) ? 0u : BSNP_ERR_NONFINITE;
+    }
+  }
+  __syncthreads();
+  // quantize labels (vs the f32 boundaries) and codes, a label byte per pair
+  for (uint32_t p = tid; 2 * p < n; p += kQThreads) {
+    uint32_t la, lb = 0;
+    codes[2 * p] = (uint8_t)quant_one(Q, s[padded(2 * p)], la);
+    if (2 * p + 1 < n) codes[2 * p + 1] = (uint8_t)quant_one(Q, s[padded(2 * p + 1)], lb);
+    labels[p] = (uint8_t)(la | (lb << 4));
+  }
+}
+
 // --------------------------------------------------------------- dequantize
 __global__ void __launch_bounds__(kQThreads)
     dequantize_kernel(const uint8_t* __restrict__ labels, const uint8_t* __restrict__ codes,
@@ -938,6 +1026,10 @@ extern "C" size_t bsnp_cluster_ws_bytes(uint64_t n, uint64_t block) {
 static int cluster_run(const float* x, uint64_t n, uint64_t block, int m,
                        bsnp_cluster_table* tables, uint8_t* labels, uint8_t* codes, void* ws,
                        size_t ws_bytes, cudaStream_t s) {
+  if (labels && n <= kTileMax && (block == 0 || block >= n) && window_enabled()) {
+    tiny_encode_kernel<<<1, kQThreads, 0, s>>>(x, (uint32_t)n, m, tables, labels, codes);
+    return launch_status("tiny_encode_kernel");
+  }
   QPlan P;
   if (!make_plan(n, block, m, P)) return BSNP_E_INVALID;
   const QWs w = carve(P, ws);
