@@ -724,6 +724,9 @@ def decode_chain(chain, device: torch.device | None = None, to_host: bool = True
             if manifest.kind == KIND_BASE:
                 model_order = []
             checks = []
+            nd = sum(1 for e in manifest.tensors
+                     if e.group == GROUP_MODEL and e.codec != CODEC_RAW)
+            sts = rt.new_status(dev, max(nd, 1))  # one status block per delta, one read
             for e in manifest.tensors:
                 if e.group != GROUP_MODEL:
                     continue
@@ -744,26 +747,29 @@ def decode_chain(chain, device: torch.device | None = None, to_host: bool = True
                         raise B.DeltaError("element count mismatch")
                     if base.dtype != torch.int16:
                         raise B.DeltaError("delta encoding requires F16 tensors")
-                    st = rt.new_status(dev)
+                    st = sts[len(checks)]
                     if n:
                         pay = dblob[po:po + 2 * n_c]
                         if po & 1:
                             pay = pay.clone()
                         B.decode_delta_async(base, dblob[mo:mo + (n + 7) // 8],
                                              pay.view(torch.int16), n_c, base, st)
-                        checks.append((st, n_c))
+                    else:
+                        st.zero_()
+                    checks.append(n_c)
                     meta[name] = (ElementType.F16, shape)
                 if manifest.kind == KIND_BASE:
                     model_order.append(e.name)
-            for st, n_c in checks:
-                (pc, flags), = rt.read_status(st)
-                B._raise_decode_flags(flags, pc, n_c)
+            if checks:
+                for (pc, flags), n_c in zip(rt.read_status(sts[:len(checks)]), checks):
+                    B._raise_decode_flags(flags, pc, n_c)
             if ci == len(chain) - 1:
-                for e in manifest.tensors:
-                    if e.group != GROUP_OPTIMIZER:
-                        continue
+                opt = [e for e in manifest.tensors if e.group == GROUP_OPTIMIZER]
+                deq = iter(_dequant_entries(mv, dblob,
+                                            [e for e in opt if e.codec == CODEC_QUANT], dev))
+                for e in opt:
                     if e.codec == CODEC_QUANT:
-                        final_opt.append(_dequant_entry(mv, dblob, e, dev))
+                        final_opt.append(next(deq))
                     else:
                         name, dtype, shape, bo, k = _parse_raw(mv, e.offset)
                         dt = torch.int16 if dtype is ElementType.F16 else torch.float32
@@ -781,32 +787,48 @@ def decode_chain(chain, device: torch.device | None = None, to_host: bool = True
                       optimizer_states=tuple(os_))
 
 
-def _dequant_entry(mv: memoryview, dblob: torch.Tensor, e: ManifestEntry, dev):
-    """BSQT record at e.offset -> dequantized device tensor; labels and codes
-    are read in place from the device copy of the blob."""
-    cur = ByteCursor(mv[e.offset:e.offset + e.length])
-    cur.magic(Q.QUANT_MAGIC)
-    (ver,) = cur.unpack("<H")
-    if ver != Q.QUANT_VERSION:
-        raise Q.QuantizerError(f"unsupported quantized-tensor version {ver}")
-    (m,) = cur.unpack("<B")
-    mean, std = cur.unpack("<ff")
-    table = Q.ClusterTable(m=m, mean=mean, std=std, boundaries=cur.unpack(f"<{m - 1}f"),
-                           scales=cur.unpack(f"<{m}f"), offsets=cur.unpack(f"<{m}f"))
-    name, shape = cur.name_and_shape()
-    n = 1
-    for s in shape:
-        n *= s
-    lo = e.offset + cur.pos
-    cur.take((n + 1) // 2)
-    co = e.offset + cur.pos
-    cur.take(n)
-    if n == 0:
-        return (name, ElementType.F32, shape, torch.empty(0, dtype=torch.float32, device=dev))
-    dq = Q.DeviceQuant(tables=rt.h2d_bytes(table.to_device_bytes(), dev),
-                       labels=dblob[lo:lo + (n + 1) // 2], codes=dblob[co:co + n],
-                       n=n, block=0, m=m)
-    return (name, ElementType.F32, shape, Q.cluster_dequantize_device(dq))
+def _dequant_entries(mv: memoryview, dblob: torch.Tensor, entries, dev) -> list:
+    """BSQT records -> dequantized device tensors.  Labels and codes are read
+    in place from the device copy of the blob; every table goes up in one
+    copy and every status comes back in one read."""
+    parsed, tabs = [], bytearray()
+    for e in entries:
+        cur = ByteCursor(mv[e.offset:e.offset + e.length])
+        cur.magic(Q.QUANT_MAGIC)
+        (ver,) = cur.unpack("<H")
+        if ver != Q.QUANT_VERSION:
+            raise Q.QuantizerError(f"unsupported quantized-tensor version {ver}")
+        (m,) = cur.unpack("<B")
+        mean, std = cur.unpack("<ff")
+        table = Q.ClusterTable(m=m, mean=mean, std=std, boundaries=cur.unpack(f"<{m - 1}f"),
+                               scales=cur.unpack(f"<{m}f"), offsets=cur.unpack(f"<{m}f"))
+        name, shape = cur.name_and_shape()
+        n = 1
+        for d in shape:
+            n *= d
+        lo = e.offset + cur.pos
+        cur.take((n + 1) // 2)
+        co = e.offset + cur.pos
+        cur.take(n)
+        parsed.append((name, shape, n, m, lo, co, len(tabs)))
+        tabs += table.to_device_bytes()
+    if not parsed:
+        return []
+    dtabs = rt.h2d_bytes(bytes(tabs), dev)
+    sts = rt.new_status(dev, len(parsed))
+    outs = []
+    for i, (name, shape, n, m, lo, co, to) in enumerate(parsed):
+        out = torch.empty(n, dtype=torch.float32, device=dev)
+        if n:
+            Q.cluster_dequantize_async(dblob[lo:lo + (n + 1) // 2], dblob[co:co + n], n, 0,
+                                       dtabs[to:to + Q.TABLE_BYTES], out, sts[i])
+        else:
+            sts[i].zero_()
+        outs.append((name, ElementType.F32, shape, out))
+    for (maxlab, flags), (_, _, _, m, _, _, _) in zip(rt.read_status(sts), parsed):
+        if flags & _lib.ERR_LABEL:
+            raise Q.QuantizerError(f"label {maxlab} >= m={m}")
+    return outs
 
 
 def write_tensors_bin(path: str, blob) -> None:
