@@ -247,11 +247,16 @@ class CheckpointEncoder:
         # CUDA graphs of the launch sequence for device-resident inputs
         # (BSNP_GRAPHS=0 disables); a key is captured the second time it is seen
         self.graphs = os.environ.get("BSNP_GRAPHS", "1") != "0"
+        # encode() into a large-enough caller buffer overlaps the encode of
+        # one group of tensors with the device-to-host copy of the previous
+        # (large checkpoints; a small one takes the CUDA-graph path whole)
+        self.pipeline_groups = int(os.environ.get("BSNP_SAVE_GROUPS", "8"))
+        self.pipeline_min_bytes = GRAPH_MAX_ARENA
         self._graphs = {}
         self._seen = set()
 
     # -- phase 1 + 2: launch every codec, one sync, build unplaced records
-    def encode_records(self, items, prev_map, kind: str):
+    def encode_records(self, items, prev_map, kind: str, allow_graph: bool = True):
         """items: [(gid, group, tensor)] in checkpoint order, tensor a
         TensorBlob or DeviceTensor; prev_map: {name: tensor or device flat}.
         Returns ([EncodedRecord], {name: device flat of the model states}).
@@ -263,7 +268,7 @@ class CheckpointEncoder:
         dev = self.dev
         host = [t for _, _, t in items if isinstance(t, TensorBlob)]
         host += [p for p in (prev_map or {}).values() if isinstance(p, TensorBlob)]
-        if host or not self.graphs:
+        if host or not self.graphs or not allow_graph:
             up = _Uploader(dev, host) if host else None
             with torch.cuda.device(dev):
                 plan = self._plan(items, prev_map, kind, up)
@@ -435,11 +440,66 @@ class CheckpointEncoder:
         returned) — page-locking a fresh multi-GB buffer per save costs
         seconds, so a training loop passes its own (e.g. two alternating
         buffers); a new one is allocated when it is missing or too small."""
+        if out is not None and out.is_pinned() and self.pipeline_groups > 1:
+            buf = out.reshape(-1).view(torch.uint8)
+            raw = sum(t.nbytes for t in list(ckpt.model_states) + list(ckpt.optimizer_states))
+            if raw > self.pipeline_min_bytes and buf.numel() >= blob_bound(ckpt):
+                return self._encode_pipelined(ckpt, prev, kind, buf)
+
         def dest(manifest, nbytes):
             if out is not None and out.is_pinned() and out.numel() >= nbytes:
                 return out.reshape(-1).view(torch.uint8)[:nbytes]
             return torch.empty(max(nbytes, 1), dtype=torch.uint8, pin_memory=True)[:nbytes]
         return self.encode_into(ckpt, prev, kind, dest)
+
+    def _encode_pipelined(self, ckpt, prev, kind, buf):
+        """encode() into a caller buffer that can hold any outcome: the
+        tensors go in a few groups, and while group g+1 is encoded the
+        records of group g (their offsets known from group g's one sync)
+        already travel to the host on a copy stream."""
+        prev_map = self._prev_map(ckpt, prev, kind)
+        items = [(i, GROUP_MODEL, t) for i, t in enumerate(ckpt.model_states)]
+        k = len(items)
+        items += [(k + i, GROUP_OPTIMIZER, t) for i, t in enumerate(ckpt.optimizer_states)]
+        total = sum(t.nbytes for _, _, t in items)
+        groups, cur, acc = [], [], 0
+        for it in items:
+            cur.append(it)
+            acc += it[2].nbytes
+            if acc >= total / self.pipeline_groups and len(groups) < self.pipeline_groups - 1:
+                groups.append(cur)
+                cur, acc = [], 0
+        if cur:
+            groups.append(cur)
+        if not hasattr(self, "_copy_stream"):
+            self._copy_stream = torch.cuda.Stream(self.dev)
+        cs, main = self._copy_stream, torch.cuda.current_stream(self.dev)
+        all_recs, offsets, model_dev, keep = [], [0], {}, []
+        # graphs only for small checkpoints (a graph per group would pin its
+        # arenas in memory)
+        small = total <= GRAPH_MAX_ARENA
+        with torch.cuda.device(self.dev):
+            for g in groups:
+                recs, md = self.encode_records(g, prev_map, kind, allow_graph=small)
+                model_dev.update(md)
+                offs = [offsets[-1]]
+                for r in recs:
+                    offs.append(offs[-1] + r.length)
+                cs.wait_stream(main)
+                with torch.cuda.stream(cs):
+                    _place_host(recs, offs, buf, 0, non_blocking=True)
+                keep.append(recs)      # the arenas live until the copies finish
+                all_recs += recs
+                offsets += offs[1:]
+            cs.synchronize()
+        base_iter = ckpt.iteration if kind == KIND_BASE else prev_iteration(prev, self.prev)
+        manifest = CheckpointManifest(
+            iteration=ckpt.iteration, kind=kind, base_iteration=base_iter,
+            tensors=tuple(ManifestEntry(r.name, r.group, r.codec, o, r.length)
+                          for r, o in zip(all_recs, offsets)))
+        if self.keep_prev:
+            self.prev = (ckpt.iteration, model_dev)
+        return manifest, buf[:offsets[-1]]
 
     def encode_into(self, ckpt: Checkpoint, prev: Checkpoint | None, kind: str, dest):
         """encode() with the landing zone chosen once the sizes are known:
@@ -482,6 +542,17 @@ class CheckpointEncoder:
         if set(pm) != {t.name for t in ckpt.model_states}:
             raise StoreError("model-state structure differs from previous checkpoint")
         return pm
+
+
+def blob_bound(ckpt: Checkpoint) -> int:
+    """An upper bound of the tensors.bin size of any encoding of `ckpt`: a
+    DELTA record is chosen only when smaller than the RAW one, and a BSQT
+    record (1.5 bytes per element plus a header) is smaller than the f32 RAW
+    record plus its 256-byte allowance."""
+    b = 0
+    for t in list(ckpt.model_states) + list(ckpt.optimizer_states):
+        b += len(tensor_header(t.name, t.dtype, t.shape)) + t.nbytes + 256
+    return b
 
 
 def _check_pair_flat(t, base_flat: torch.Tensor) -> None:
@@ -711,16 +782,24 @@ def decode_chain(chain, device: torch.device | None = None, to_host: bool = True
             model_order.append(t.name)
     with torch.cuda.device(dev):
         for ci, (manifest, blob) in enumerate(chain):
+            # only the final checkpoint's optimizer states are restored: an
+            # earlier link needs just the span of its model records
+            need = None
+            if ci < len(chain) - 1:
+                need = max((e.offset + e.length for e in manifest.tensors
+                            if e.group == GROUP_MODEL), default=0)
             if isinstance(blob, torch.Tensor) and blob.is_pinned():
                 pin = blob.reshape(-1).view(torch.uint8)   # e.g. CheckpointEncoder output
                 mv = memoryview(pin.numpy())
             else:
                 mv = memoryview(blob).cast("B")
-                pin = torch.empty(max(len(mv), 1), dtype=torch.uint8, pin_memory=True)
-                pin.numpy()[:len(mv)] = np.frombuffer(mv, dtype=np.uint8)
-            dblob = torch.empty(len(mv), dtype=torch.uint8, device=dev)
-            if len(mv):
-                dblob.copy_(pin[:len(mv)], non_blocking=True)
+                k = len(mv) if need is None else min(need, len(mv))
+                pin = torch.empty(max(k, 1), dtype=torch.uint8, pin_memory=True)
+                pin.numpy()[:k] = np.frombuffer(mv[:k], dtype=np.uint8)
+            need = len(mv) if need is None else min(need, len(mv))
+            dblob = torch.empty(need, dtype=torch.uint8, device=dev)
+            if need:
+                dblob.copy_(pin[:need], non_blocking=True)
             if manifest.kind == KIND_BASE:
                 model_order = []
             checks = []

@@ -268,3 +268,34 @@ def test_graph_replay_of_repeated_saves(dev, checkpoint_golden, golden_index):
                 c0, S.KIND_DELTA)
             assert man.to_bytes() == ref.to_bytes()
     assert len(enc._graphs) == 1
+
+
+@pytest.mark.parametrize("groups", [1, 2, 3, 8])
+def test_pipelined_save_into_caller_buffer(dev, checkpoint_golden, golden_index, groups):
+    """encode() into a pinned buffer that can hold any outcome overlaps the
+    encode of one group of tensors with the copy-out of the previous one:
+    same blob and manifest as the reference for any group count."""
+    g, meta = checkpoint_golden, golden_index["checkpoint"]
+    c0, c1 = _golden_ckpts(g, meta)
+    enc = S.CheckpointEncoder(dev, clusters=16, keep_prev=False)
+    enc.pipeline_groups = groups
+    enc.pipeline_min_bytes = 0      # the golden checkpoint is small: force the path
+    buf = torch.empty(S.blob_bound(c1) + 7, dtype=torch.uint8, pin_memory=True)
+    for ck, prev, kind, bkey, mkey in ((c0, None, S.KIND_BASE, "blob0", "manifest0"),
+                                       (c1, c0, S.KIND_DELTA, "blob1", "manifest1")):
+        man, out = enc.encode(ck, prev, kind, out=buf)
+        assert out.numpy().tobytes() == g[bkey].tobytes()
+        assert man.to_bytes() == g[mkey].tobytes()
+
+
+def test_chain_replay_uploads_only_needed_spans(dev, checkpoint_golden, golden_index):
+    """Earlier links of a chain contribute only their model records: a base
+    blob truncated after its model section decodes to the same checkpoint."""
+    g = checkpoint_golden
+    m0 = S.CheckpointManifest.from_bytes(g["manifest0"].tobytes())
+    m1 = S.CheckpointManifest.from_bytes(g["manifest1"].tobytes())
+    end = max(e.offset + e.length for e in m0.tensors if e.group == S.GROUP_MODEL)
+    full = S.decode_chain([(m0, g["blob0"].tobytes()), (m1, g["blob1"].tobytes())])
+    cut = S.decode_chain([(m0, g["blob0"].tobytes()[:end]), (m1, g["blob1"].tobytes())])
+    assert [t.data for t in full.model_states] == [t.data for t in cut.model_states]
+    assert [t.data for t in full.optimizer_states] == [t.data for t in cut.optimizer_states]

@@ -96,10 +96,12 @@ def main():
         return out, time.perf_counter() - t
 
     # a training loop keeps its pinned save buffers (page-locking GBs per save
-    # would dominate): one untimed save pair sizes them
-    m0, b0 = enc.encode(c0, None, S.KIND_BASE)
-    m1, b1 = enc.encode(c1, None, S.KIND_DELTA)
-    buf0, buf1 = b0, b1
+    # would dominate), sized for any outcome (store.blob_bound) so the save
+    # can stream groups of records out while later groups are encoded
+    buf0 = torch.empty(S.blob_bound(c0), dtype=torch.uint8, pin_memory=True)
+    buf1 = torch.empty(S.blob_bound(c1), dtype=torch.uint8, pin_memory=True)
+    m0, b0 = enc.encode(c0, None, S.KIND_BASE, out=buf0)
+    m1, b1 = enc.encode(c1, None, S.KIND_DELTA, out=buf1)
     res = {}
     out = None
     for _ in range(args.reps):
