@@ -50,6 +50,8 @@ def parse_args():
     ap.add_argument("--cpu-elems-per-core", type=int, default=1 << 23)
     ap.add_argument("--no-c2", action="store_true",
                     help="skip the C2 cluster-quantizer measurement")
+    ap.add_argument("--no-c0", action="store_true",
+                    help="skip the whole-checkpoint line (BASELINE configs[0], GPT-2-small)")
     ap.add_argument("--c2-log2n", type=int, default=30)
     ap.add_argument("--c2-block", type=int, default=1 << 20)
     return ap.parse_args()
@@ -296,6 +298,7 @@ def run_b200(args, rank: int, world: int, local_rank: int):
         e2e = run_e2e(args, base, cur, k, dev, world)
     del base, cur, mask, payload, out
     c2 = None if args.no_c2 else run_c2(args, dev, world)
+    c0 = None if (args.no_c0 or world > 1) else run_c0(dev)
 
     if rank != 0:
         return
@@ -330,9 +333,57 @@ def run_b200(args, rank: int, world: int, local_rank: int):
         line["e2e"] = e2e
     if c2:
         line["c2_cluster_quant"] = c2
+    if c0:
+        line["c0_checkpoint"] = c0
     if world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(args.p, args.cpu_elems_per_core)
     print(json.dumps(line), flush=True)
+
+
+def run_c0(dev, reps: int = 3):
+    """BASELINE configs[0]: a GPT-2-small checkpoint pair (bf16 weights, fp32
+    Adam m/v; tools/bench_checkpoint.py recipe) saved as base + delta through
+    store.CheckpointEncoder into reused pinned buffers and restored with
+    decode_chain (blobs H2D, chain replay, dequantize).  GB/s = raw bytes /
+    wall time per call (device work and PCIe copies inside)."""
+    import torch
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from bench_checkpoint import generate
+    from paper_2511_12376_b200 import store as S
+    c0, c1 = generate("C0", dev)
+    raw = sum(t.nbytes for t in c1.model_states + c1.optimizer_states)
+    enc = S.CheckpointEncoder(dev, clusters=16)
+    bufs = [torch.empty(S.blob_bound(c), dtype=torch.uint8, pin_memory=True) for c in (c0, c1)]
+    best = {}
+    for _ in range(reps + 1):
+        t = []
+        for fn in (lambda: enc.encode(c0, None, S.KIND_BASE, out=bufs[0]),
+                   lambda: enc.encode(c1, None, S.KIND_DELTA, out=bufs[1])):
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            res = fn()
+            torch.cuda.synchronize(dev)
+            t.append((time.perf_counter() - t0, res))
+        chain = [t[0][1], t[1][1]]
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        out = S.decode_chain(chain, to_host=False)
+        torch.cuda.synchronize(dev)
+        tl = time.perf_counter() - t0
+        del out
+        for k, v in (("save_base_s", t[0][0]), ("save_delta_s", t[1][0]), ("load_s", tl)):
+            best[k] = min(best.get(k, 1e9), v)
+    blob = chain[1][1].numel()
+    return {"workload": "C0: GPT-2-small checkpoint (124.4M params, 148 tensors; bf16 weights, "
+                        "fp32 Adam m/v, m = 16), base + delta save, chain restore",
+            "raw_bytes": raw, "delta_blob_bytes": blob,
+            "compression_ratio": round(raw / blob, 4),
+            "save_delta_gbs": round(raw / best["save_delta_s"] / 1e9, 2),
+            "save_base_gbs": round(raw / best["save_base_s"] / 1e9, 2),
+            "load_gbs": round(raw / best["load_s"] / 1e9, 2),
+            **{k: round(v, 4) for k, v in best.items()},
+            "timing": "host wall clock per call, device-resident inputs, pinned host "
+                      "outputs, best of 3 after one untimed pair"}
 
 
 def run_c2(args, dev, world):
