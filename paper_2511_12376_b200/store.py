@@ -798,8 +798,7 @@ def decode_chain(chain, device: torch.device | None = None, to_host: bool = True
                 pin.numpy()[:k] = np.frombuffer(mv[:k], dtype=np.uint8)
             need = len(mv) if need is None else min(need, len(mv))
             dblob = torch.empty(need, dtype=torch.uint8, device=dev)
-            if need:
-                dblob.copy_(pin[:need], non_blocking=True)
+            ready = _ChunkedUpload(pin, dblob, need, dev)
             if manifest.kind == KIND_BASE:
                 model_order = []
             checks = []
@@ -809,6 +808,7 @@ def decode_chain(chain, device: torch.device | None = None, to_host: bool = True
             for e in manifest.tensors:
                 if e.group != GROUP_MODEL:
                     continue
+                ready(e.offset + e.length)
                 if e.codec == CODEC_RAW:
                     name, dtype, shape, bo, k = _parse_raw(mv, e.offset)
                     dt = torch.int16 if dtype is ElementType.F16 else torch.float32
@@ -842,17 +842,22 @@ def decode_chain(chain, device: torch.device | None = None, to_host: bool = True
             if checks:
                 for (pc, flags), n_c in zip(rt.read_status(sts[:len(checks)]), checks):
                     B._raise_decode_flags(flags, pc, n_c)
+            if ci < len(chain) - 1:
+                ready.finish()
             if ci == len(chain) - 1:
                 opt = [e for e in manifest.tensors if e.group == GROUP_OPTIMIZER]
                 deq = iter(_dequant_entries(mv, dblob,
-                                            [e for e in opt if e.codec == CODEC_QUANT], dev))
+                                            [e for e in opt if e.codec == CODEC_QUANT], dev,
+                                            ready))
                 for e in opt:
                     if e.codec == CODEC_QUANT:
                         final_opt.append(next(deq))
                     else:
+                        ready(e.offset + e.length)
                         name, dtype, shape, bo, k = _parse_raw(mv, e.offset)
                         dt = torch.int16 if dtype is ElementType.F16 else torch.float32
                         final_opt.append((name, dtype, shape, dblob[bo:bo + k].clone().view(dt)))
+                ready.finish()
         if not model_order:
             model_order = list(model)
         final = chain[-1][0]
@@ -866,7 +871,57 @@ def decode_chain(chain, device: torch.device | None = None, to_host: bool = True
                       optimizer_states=tuple(os_))
 
 
-def _dequant_entries(mv: memoryview, dblob: torch.Tensor, entries, dev) -> list:
+class _ChunkedUpload:
+    """Host blob -> device copy in a few chunks on a copy stream; calling
+    the object with a byte end makes the current stream wait for the chunk
+    holding it, so records are decoded while later chunks are in flight."""
+
+    CHUNKS = 8
+
+    def __init__(self, pin: torch.Tensor, dblob: torch.Tensor, need: int, dev):
+        self.events, self.bounds, self.waited = [], [], -1
+        if not need:
+            return
+        self.main = torch.cuda.current_stream(dev)
+        cs = _copy_stream(dev)
+        cs.wait_stream(self.main)
+        step = max((need + self.CHUNKS - 1) // self.CHUNKS, 1 << 20)
+        with torch.cuda.stream(cs):
+            for a in range(0, need, step):
+                b = min(a + step, need)
+                dblob[a:b].copy_(pin[a:b], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(cs)
+                self.events.append(ev)
+                self.bounds.append(b)
+        dblob.record_stream(cs)
+
+    def __call__(self, end: int) -> None:
+        if self.waited >= 0 and self.bounds[self.waited] >= end:
+            return
+        for i in range(self.waited + 1, len(self.bounds)):
+            self.main.wait_event(self.events[i])
+            self.waited = i
+            if self.bounds[i] >= end:
+                break
+
+    def finish(self) -> None:
+        """The current stream waits for every chunk."""
+        if self.bounds:
+            self(self.bounds[-1])
+
+
+_COPY_STREAMS: dict = {}
+
+
+def _copy_stream(dev) -> torch.cuda.Stream:
+    key = torch.device(dev).index
+    if key not in _COPY_STREAMS:
+        _COPY_STREAMS[key] = torch.cuda.Stream(torch.device(dev))
+    return _COPY_STREAMS[key]
+
+
+def _dequant_entries(mv: memoryview, dblob: torch.Tensor, entries, dev, ready=None) -> list:
     """BSQT records -> dequantized device tensors.  Labels and codes are read
     in place from the device copy of the blob; every table goes up in one
     copy and every status comes back in one read."""
@@ -898,6 +953,8 @@ def _dequant_entries(mv: memoryview, dblob: torch.Tensor, entries, dev) -> list:
     outs = []
     for i, (name, shape, n, m, lo, co, to) in enumerate(parsed):
         out = torch.empty(n, dtype=torch.float32, device=dev)
+        if ready is not None:
+            ready(co + n)
         if n:
             Q.cluster_dequantize_async(dblob[lo:lo + (n + 1) // 2], dblob[co:co + n], n, 0,
                                        dtabs[to:to + Q.TABLE_BYTES], out, sts[i])
