@@ -11,7 +11,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 900 python bench.py > gpurun_out/bench_$tag.json 2> gpurun_out/bench_$tag.err
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_$tag.json 2> gpurun_out/bench_ref_$tag.err
 if [ "${NCU:-1}" = 1 ]; then
-CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu"
+CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-c0"
 timeout 300 $CMD > gpurun_out/plain_$tag.log 2>&1 && \
   timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file gpurun_out/launches_$tag.csv $CMD > gpurun_out/ncu_launch_$tag.log 2>&1 && \
