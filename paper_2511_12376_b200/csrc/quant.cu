@@ -323,9 +323,14 @@ __global__ void __launch_bounds__(kQThreads)
                     double* __restrict__ partials) {
   __shared__ __align__(16) float s[kSmemFloats];
   __shared__ Heap H;
-  const double m = kVar ? mu[locate(P, blockIdx.x).u] : 0.0;
-  const double v = tree_tile<kVar>(x, P, blockIdx.x, m, s, H, policy_evict_first());
-  if (threadIdx.x == 0) partials[blockIdx.x] = v;
+  // the variance pass walks the tiles backwards: its first tiles are the
+  // last ones the sum pass read, still in L2 (the labels pass then walks
+  // forwards again, the codes pass backwards); only the codes pass, the
+  // last reader of x, marks its lines evict-first
+  const uint64_t tile = kVar ? P.total_tiles - 1 - blockIdx.x : blockIdx.x;
+  const double m = kVar ? mu[locate(P, tile).u] : 0.0;
+  const double v = tree_tile<kVar>(x, P, tile, m, s, H, policy_evict_normal());
+  if (threadIdx.x == 0) partials[tile] = v;
 }
 
 // Sum of the 2^D partials of one unit as a perfect binary tree.

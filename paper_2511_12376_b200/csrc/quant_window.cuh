@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(kQThreads)
     fit_label_kernel(const float* __restrict__ x, QPlan P, UGrid* __restrict__ ug,
                      uint8_t* __restrict__ labels) {
   __shared__ __align__(16) WSmem S;
-  label_chunk(x, P, chunk_of(P, blockIdx.x), ug, labels, S, policy_evict_first());
+  label_chunk(x, P, chunk_of(P, blockIdx.x), ug, labels, S, policy_evict_normal());
 }
 
 // one warp per unit: extremes from the candidates, or mark the exact round;
@@ -556,5 +556,7 @@ __global__ void __launch_bounds__(kQThreads)
                           const bsnp_cluster_table* __restrict__ tables,
                           const uint8_t* __restrict__ labels, uint8_t* __restrict__ codes) {
   __shared__ CodesSmem cs;
-  codes_chunk(x, P, chunk_of(P, blockIdx.x), tables, labels, codes, cs, policy_evict_first());
+  const uint64_t nch = (uint64_t)(P.nunits - 1) * P.C_full + P.C_last;
+  codes_chunk(x, P, chunk_of(P, nch - 1 - blockIdx.x), tables, labels, codes, cs,
+              policy_evict_first());
 }
