@@ -378,15 +378,23 @@ __device__ __forceinline__ void unit_shape(const QPlan& P, uint32_t u, uint32_t&
 
 // Mean (kVar = false) or std + table header + fit thresholds (kVar = true) of
 // unit u from its tile partials; CTA-wide (sv: kQThreads doubles of smem).
+constexpr uint32_t kPreGroup = 1024;  // partials per pre-reduction CTA
+constexpr int kPreShift = 10;
+
 template <bool kVar>
 __device__ __forceinline__ void combine_unit(const QPlan& P, uint32_t u,
                                              const double* partials, double* mu, float* fthr,
                                              bsnp_cluster_table* tables, double* sdv,
-                                             double* sv) {
+                                             double* sv, const double* partials2 = nullptr) {
   uint32_t T;
   uint64_t len;
   unit_shape(P, u, T, len);
-  const double S = combine_perfect(partials + (uint64_t)u * P.T_full, T, sv);
+  // with T > kPreGroup the partials were pre-reduced in groups of kPreGroup
+  // (pre_combine_kernel): the same perfect tree, one level set at a time
+  const int sh = T > kPreGroup ? kPreShift : 0;
+  const uint32_t Tg = T >> sh;
+  const double S = combine_perfect((sh ? partials2 : partials) + ((uint64_t)u * P.T_full >> sh),
+                                   Tg, sv);
   if (threadIdx.x != 0) return;
   const double mean = __ddiv_rn(__dadd_rn(0.0, S), (double)len);  // np.mean
   bsnp_cluster_table& tb = tables[u];
@@ -421,9 +429,45 @@ template <bool kVar>
 __global__ void __launch_bounds__(kQThreads)
     fit_combine_kernel(QPlan P, const double* __restrict__ partials, double* __restrict__ mu,
                        float* __restrict__ fthr, bsnp_cluster_table* __restrict__ tables,
-                       double* __restrict__ sdv = nullptr) {
+                       double* __restrict__ sdv = nullptr,
+                       const double* __restrict__ partials2 = nullptr) {
   __shared__ double sv[kQThreads];
-  combine_unit<kVar>(P, blockIdx.x, partials, mu, fthr, tables, sdv, sv);
+  combine_unit<kVar>(P, blockIdx.x, partials, mu, fthr, tables, sdv, sv, partials2);
+}
+
+// Units with more than kPreGroup tiles (per-tensor units above 2^23
+// elements): each CTA folds kPreGroup consecutive tile partials - a perfect
+// sub-tree of the unit's perfect tree - so the per-unit combine folds
+// T / kPreGroup values instead of T (a 2^30-element unit: 181 -> ~10 us).
+__global__ void __launch_bounds__(kQThreads)
+    pre_combine_kernel(QPlan P, const double* __restrict__ partials,
+                       double* __restrict__ partials2) {
+  __shared__ double v[kPreGroup];
+  const uint64_t g = blockIdx.x;  // group index over all units (T_full-strided)
+  const uint64_t gpu = P.T_full >> kPreShift;  // groups per full unit
+  const uint32_t u = (uint32_t)(g / gpu);
+  const uint32_t T = u == P.nunits - 1 ? P.T_last : P.T_full;
+  if (((g % gpu) << kPreShift) >= T) return;  // the last unit may have fewer tiles
+  const double* src = partials + (g << kPreShift);
+  for (int i = threadIdx.x; i < (int)kPreGroup; i += kQThreads) v[i] = src[i];
+  constexpr int kPer = kPreGroup / 2 / kQThreads;  // pairs per thread at the first level
+  for (uint32_t w = kPreGroup / 2; w >= 1; w /= 2) {
+    __syncthreads();
+    double a[kPer];
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const uint32_t i = threadIdx.x + q * kQThreads;
+      if (i < w) a[q] = __dadd_rn(v[2 * i], v[2 * i + 1]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const uint32_t i = threadIdx.x + q * kQThreads;
+      if (i < w) v[i] = a[q];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) partials2[g] = v[0];
 }
 
 template <bool kLut>
@@ -927,6 +971,7 @@ bool make_plan(uint64_t n, uint64_t block, int m, QPlan& P) {
 struct UGrid;
 struct QWs {
   double* partials;  // total_tiles
+  double* partials2; // nunits * (T_full / kPreGroup): pre-reduced partials (T_full > kPreGroup)
   double* mu;        // nunits
   float* fthr;       // nunits * 16
   int* tile_mm;      // total_tiles * 32
@@ -946,6 +991,7 @@ QWs carve(const QPlan& P, void* ws) {
     return r;
   };
   w.partials = (double*)take(8 * P.total_tiles);
+  w.partials2 = (double*)take(8 * (size_t)P.nunits * (P.T_full >> kPreShift) + 8);
   w.mu = (double*)take(8 * (size_t)P.nunits);
   w.fthr = (float*)take(64 * (size_t)P.nunits);
   w.tile_mm = (int*)take(128 * P.total_tiles);
@@ -956,18 +1002,33 @@ QWs carve(const QPlan& P, void* ws) {
   return w;
 }
 
+// the per-unit combine, pre-reducing groups of kPreGroup partials for units
+// with more tiles
+template <bool kVar>
+int launch_combine(const QPlan& P, bsnp_cluster_table* tables, const QWs& w, cudaStream_t s) {
+  int rc;
+  const double* p2 = nullptr;
+  if (P.T_full > kPreGroup) {
+    pre_combine_kernel<<<(unsigned)(P.nunits * (P.T_full >> kPreShift)), kQThreads, 0, s>>>(
+        P, w.partials, w.partials2);
+    if ((rc = launch_status("pre_combine_kernel"))) return rc;
+    p2 = w.partials2;
+  }
+  fit_combine_kernel<kVar><<<P.nunits, kQThreads, 0, s>>>(P, w.partials, w.mu, w.fthr, tables,
+                                                          kVar ? w.sd : nullptr, p2);
+  return launch_status(kVar ? "fit_combine_kernel<std>" : "fit_combine_kernel<mean>");
+}
+
 int run_fit(const float* x, const QPlan& P, bsnp_cluster_table* tables, const QWs& w,
             cudaStream_t s) {
   int rc;
   const unsigned tiles = (unsigned)P.total_tiles;
   fit_tree_kernel<false><<<tiles, kQThreads, 0, s>>>(x, P, w.mu, w.partials);
   if ((rc = launch_status("fit_tree_kernel<sum>"))) return rc;
-  fit_combine_kernel<false><<<P.nunits, kQThreads, 0, s>>>(P, w.partials, w.mu, w.fthr, tables);
-  if ((rc = launch_status("fit_combine_kernel<mean>"))) return rc;
+  if ((rc = launch_combine<false>(P, tables, w, s))) return rc;
   fit_tree_kernel<true><<<tiles, kQThreads, 0, s>>>(x, P, w.mu, w.partials);
   if ((rc = launch_status("fit_tree_kernel<var>"))) return rc;
-  fit_combine_kernel<true><<<P.nunits, kQThreads, 0, s>>>(P, w.partials, w.mu, w.fthr, tables);
-  if ((rc = launch_status("fit_combine_kernel<std>"))) return rc;
+  if ((rc = launch_combine<true>(P, tables, w, s))) return rc;
   fit_minmax_kernel<<<tiles, kQThreads, 0, s>>>(x, P, w.fthr, w.tile_mm);
   if ((rc = launch_status("fit_minmax_kernel"))) return rc;
   fit_finalize_kernel<<<P.nunits, kQThreads, 0, s>>>(P, w.tile_mm, tables);
@@ -991,13 +1052,10 @@ int run_window(const float* x, const QPlan& P, bsnp_cluster_table* tables, uint8
   const unsigned tiles = (unsigned)P.total_tiles;
   fit_tree_kernel<false><<<tiles, kQThreads, 0, s>>>(x, P, w.mu, w.partials);
   if ((rc = launch_status("fit_tree_kernel<sum>"))) return rc;
-  fit_combine_kernel<false><<<P.nunits, kQThreads, 0, s>>>(P, w.partials, w.mu, w.fthr, tables);
-  if ((rc = launch_status("fit_combine_kernel<mean>"))) return rc;
+  if ((rc = launch_combine<false>(P, tables, w, s))) return rc;
   fit_tree_kernel<true><<<tiles, kQThreads, 0, s>>>(x, P, w.mu, w.partials);
   if ((rc = launch_status("fit_tree_kernel<var>"))) return rc;
-  fit_combine_kernel<true><<<P.nunits, kQThreads, 0, s>>>(P, w.partials, w.mu, w.fthr, tables,
-                                                           w.sd);
-  if ((rc = launch_status("fit_combine_kernel<std>"))) return rc;
+  if ((rc = launch_combine<true>(P, tables, w, s))) return rc;
   fit_grid_kernel<<<P.nunits, kQThreads, 0, s>>>(P, w.mu, w.sd, w.ug, w.need + P.nunits);
   if ((rc = launch_status("fit_grid_kernel"))) return rc;
   const unsigned chunks = (unsigned)((uint64_t)(P.nunits - 1) * P.C_full + P.C_last);

@@ -110,22 +110,30 @@ __device__ __forceinline__ void grid_unit(const QPlan& P, uint32_t u, double m0,
     G.gi = gi;
     G.c0 = c0;
     s_delta = __double2float_ru(__ddiv_rn(__dmul_rn((double)kWDeltaNum, sd), (double)len));
-    G.delta = s_delta;
     G.gmax = 0;
     G.gmin_c = 0;
   }
   __syncthreads();
+  float f = __int_as_float(0x7f800000), r = f;
   if (tid < 16) {
-    float f = __int_as_float(0x7f800000), r = f;
     if (tid < m - 1) {
       const double b64 = __dadd_rn(m0, __dmul_rn(sd, kNdtri[m][tid]));
       f = __double2float_rd(b64);
       r = __double2float_rn(b64);
+      // a window narrower than a few f32 spacings at F would miss pred/succ
+      // of large units (2^30 elements: 80 sd / n is below one ulp of F)
+      const float af = fabsf(f);
+      if (isfinite(af)) atomicMax(reinterpret_cast<int*>(&s_delta),
+                                  __float_as_int(4.0f * (nextafterf(af, INFINITY) - af)));
     }
     G.F[tid] = f;
     G.B32[tid] = r;
     G.lo[tid] = 0;
     G.hi_c[tid] = 0;
+  }
+  __syncthreads();
+  if (tid == 0) G.delta = s_delta;
+  if (tid < 16) {
     binB[tid] = tid < m - 1 ? (int)w_bin(r, s_gi, s_c0) : 0x3fffffff;
     // bins meeting the window around F_k (monotone bins: |v - F| < delta
     // implies bin(F - delta) <= bin(v) <= bin(F + delta))

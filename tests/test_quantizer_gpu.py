@@ -348,3 +348,16 @@ def test_many_units_vs_oracle(dev, log2b, units, tail, dist, m):
         x[2 * block:3 * block] = -0.75    # a constant block (sd = 0)
     dq = Q.cluster_encode_device(_f32(x, dev), m, block)
     _check_units(x, m, block, dq)
+
+
+@pytest.mark.parametrize("n,block", [((1 << 24) + 12345, 0), (2 * (1 << 23) + 5000, 1 << 23)])
+def test_large_units_pre_reduced_combine(dev, n, block):
+    """Units of more than 1024 tree tiles (2^23+ elements) fold their tile
+    partials in groups of 1024 before the per-unit combine (the same perfect
+    tree); a ragged last unit of few tiles takes the direct combine.  Tables,
+    labels and codes bit-exact vs the oracle."""
+    from paper_2511_12376_b200 import quantizer as Q
+    rng = np.random.default_rng(n)
+    x = (rng.standard_normal(n) * 1e-3).astype(np.float32)
+    dq = Q.cluster_encode_device(_f32(x, dev), 16, block)
+    _check_units(x, 16, block, dq)
