@@ -657,8 +657,17 @@ template <bool kLut>
 __device__ __forceinline__ void quant_loop(const LabelLut& L, const QuantParams& Q,
                                            const float2* qp, const float* src, uint8_t* cdst,
                                            uint8_t* ldst, uint32_t nv) {
-  for (uint32_t i = threadIdx.x; i < nv; i += kQThreads) {
-    const float4 v4 = ld_stream_f4(src + 4 * i);
+  constexpr int kB = 4;  // vectors per thread in flight (the loop was load-latency bound)
+  for (uint32_t i0 = threadIdx.x; i0 < nv; i0 += kB * kQThreads) {
+    float4 vb[kB];
+#pragma unroll
+    for (int b = 0; b < kB; ++b)
+      if (i0 + b * kQThreads < nv) vb[b] = ld_stream_f4(src + 4 * (i0 + b * kQThreads));
+#pragma unroll
+    for (int b = 0; b < kB; ++b) {
+    const uint32_t i = i0 + b * kQThreads;
+    if (i >= nv) break;
+    const float4 v4 = vb[b];
     const float v[4] = {v4.x, v4.y, v4.z, v4.w};
     uint32_t c[4], code[4];
     bool amb = false;
@@ -684,6 +693,7 @@ __device__ __forceinline__ void quant_loop(const LabelLut& L, const QuantParams&
         code[0] | (code[1] << 8) | (code[2] << 16) | (code[3] << 24);
     *reinterpret_cast<uint16_t*>(ldst + 2 * i) =
         (uint16_t)(c[0] | (c[1] << 4) | (c[2] << 8) | (c[3] << 12));
+    }
   }
 }
 
@@ -694,19 +704,33 @@ __global__ void __launch_bounds__(kQThreads)
   __shared__ QuantParams Q;
   __shared__ LabelLut L;
   __shared__ float2 qp[16];
-  const TileRef r = locate(P, blockIdx.x);
-  load_quant_params(tables[r.u], Q);
+  // one CTA per kDqChunk-element chunk of a unit (one parameter / LUT setup
+  // per 64 Ki elements)
+  const uint64_t full_chunks = (uint64_t)(P.nunits - 1) * P.C_full;
+  uint32_t u;
+  uint64_t c0, ulen;
+  if (blockIdx.x < full_chunks) {
+    u = (uint32_t)(blockIdx.x / P.C_full);
+    c0 = (blockIdx.x % P.C_full) * kDqChunk;
+    ulen = P.block;
+  } else {
+    u = P.nunits - 1;
+    c0 = (blockIdx.x - full_chunks) * kDqChunk;
+    ulen = P.last_len;
+  }
+  load_quant_params(tables[u], Q);
   __syncthreads();
   if (threadIdx.x < 16) {
     L.bnd[threadIdx.x] = Q.bnd[threadIdx.x];
     qp[threadIdx.x] = make_float2(Q.off[threadIdx.x], Q.rcp[threadIdx.x]);
   }
   __syncthreads();
-  lut_build_cta(L, (int)tables[r.u].m);
-  const float* src = x + r.ustart + r.off;
-  uint8_t* cdst = codes + r.ustart + r.off;
-  uint8_t* ldst = labels + (uint64_t)r.u * (P.block / 2) + r.off / 2;
-  const uint32_t size = (uint32_t)r.size;
+  lut_build_cta(L, (int)tables[u].m);
+  const uint64_t ustart = (uint64_t)u * P.block;
+  const float* src = x + ustart + c0;
+  uint8_t* cdst = codes + ustart + c0;
+  uint8_t* ldst = labels + (uint64_t)u * (P.block / 2) + c0 / 2;
+  const uint32_t size = (uint32_t)((c0 + kDqChunk < ulen ? c0 + kDqChunk : ulen) - c0);
   const bool vec = (((uintptr_t)src & 15) | ((uintptr_t)cdst & 3) | ((uintptr_t)ldst & 1)) == 0;
   const uint32_t nv = vec ? size / 4 : 0;
   if (L.ok) quant_loop<true>(L, Q, qp, src, cdst, ldst, nv);
@@ -1100,7 +1124,8 @@ static int cluster_run(const float* x, uint64_t n, uint64_t block, int m,
   if (window_enabled()) return run_window(x, P, tables, labels, codes, w, s);
   int rc = run_fit(x, P, tables, w, s);
   if (rc || !labels) return rc;
-  quantize_kernel<<<(unsigned)P.total_tiles, kQThreads, 0, s>>>(x, P, tables, labels, codes);
+  quantize_kernel<<<(unsigned)((uint64_t)(P.nunits - 1) * P.C_full + P.C_last), kQThreads, 0,
+                    s>>>(x, P, tables, labels, codes);
   return launch_status("quantize_kernel");
 }
 
@@ -1124,8 +1149,8 @@ extern "C" int bsnp_cluster_quantize(const float* x, uint64_t n, uint64_t block,
   if (((uintptr_t)x & 3) || ((uintptr_t)tables & 15)) return BSNP_E_ALIGN;
   (void)ws;
   (void)ws_bytes;
-  quantize_kernel<<<(unsigned)P.total_tiles, kQThreads, 0, (cudaStream_t)stream>>>(
-      x, P, tables, labels, codes);
+  quantize_kernel<<<(unsigned)((uint64_t)(P.nunits - 1) * P.C_full + P.C_last), kQThreads, 0,
+                    (cudaStream_t)stream>>>(x, P, tables, labels, codes);
   return launch_status("quantize_kernel");
 }
 
