@@ -16,7 +16,7 @@ timeout 300 $CMD > gpurun_out/plain_$tag.log 2>&1 && \
   timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file gpurun_out/launches_$tag.csv $CMD > gpurun_out/ncu_launch_$tag.log 2>&1 && \
   timeout 1200 ncu --set full --clock-control none --import-source on \
-    -k 'regex:delta_(encode_ws|decode_tma|offsets)|fit_label|quantize_codes|fit_tree|dequantize' -c 10 -f -o gpurun_out/prof_$tag $CMD \
+    -k "regex:delta_(encode_ws|decode_tma|offsets)" -c 3 -f -o gpurun_out/prof_$tag $CMD \
     > gpurun_out/ncu_full_$tag.log 2>&1
 fi
 echo done
