@@ -252,6 +252,8 @@ class CheckpointEncoder:
         # (large checkpoints; a small one takes the CUDA-graph path whole)
         self.pipeline_groups = int(os.environ.get("BSNP_SAVE_GROUPS", "8"))
         self.pipeline_min_bytes = GRAPH_MAX_ARENA
+        # side streams the per-tensor launch chains are spread over
+        self.side_streams = int(os.environ.get("BSNP_SIDE_STREAMS", "8"))
         self._graphs = {}
         self._seen = set()
 
@@ -363,29 +365,51 @@ class CheckpointEncoder:
         code_a = torch.empty(max(n_code, 1), dtype=torch.uint8, device=dev)
         tab_a = torch.empty(max(n_tab, 1) * Q.TABLE_BYTES, dtype=torch.uint8, device=dev)
         deltas, quants, di = [], [], 0
+        # independent tensors go round-robin over a few side streams, so the
+        # short kernels of small tensors overlap instead of queueing (in a
+        # recorded graph: parallel branches)
+        main = torch.cuda.current_stream(dev)
+        if not hasattr(self, "_side"):
+            self._side = [torch.cuda.Stream(dev) for _ in range(self.side_streams)]
+        for ss in self._side:
+            ss.wait_stream(main)
+        launched = 0
         for p in plan["steps"]:
-            if p[0] == "delta":
-                _, gid, t, flat, bflat, mo, po = p
-                n = t.num_elements
-                if n:
-                    B.encode_delta_async(bflat, flat, mask_a[mo:mo + (n + 7) // 8],
-                                         pay_a[po:po + n], st[di])
-                else:
-                    st[di].zero_()
-                deltas.append((p, di))
-                di += 1
-            elif p[0] == "quant":
-                _, gid, t, flat, lo, co, to = p
-                n = t.num_elements
-                u = Q.num_units(n, self.block)
-                Q.cluster_encode_async(flat, self.clusters, self.block,
-                                       tab_a[to * Q.TABLE_BYTES:(to + u) * Q.TABLE_BYTES],
-                                       lab_a[lo:lo + Q.unit_label_bytes(n, self.block)],
-                                       code_a[co:co + n])
-                quants.append(p)
+            if p[0] == "raw":
+                continue
+            with torch.cuda.stream(self._side[launched % len(self._side)]):
+                di = self._launch_step(p, st, di, deltas, quants, mask_a, pay_a, lab_a, code_a,
+                                       tab_a)
+            launched += 1
+        for ss in self._side:
+            main.wait_stream(ss)
         tab_h.copy_(tab_a, non_blocking=True)
         return {"plan": plan, "arenas": (mask_a, pay_a, lab_a, code_a, tab_a),
                 "tab_h": tab_h, "st": st, "deltas": deltas, "quants": quants}
+
+    def _launch_step(self, p, st, di, deltas, quants, mask_a, pay_a, lab_a, code_a, tab_a):
+        """One tensor's codec launches on the current stream; returns the next
+        delta status index."""
+        if p[0] == "delta":
+            _, gid, t, flat, bflat, mo, po = p
+            n = t.num_elements
+            if n:
+                B.encode_delta_async(bflat, flat, mask_a[mo:mo + (n + 7) // 8],
+                                     pay_a[po:po + n], st[di])
+            else:
+                st[di].zero_()
+            deltas.append((p, di))
+            di += 1
+        elif p[0] == "quant":
+            _, gid, t, flat, lo, co, to = p
+            n = t.num_elements
+            u = Q.num_units(n, self.block)
+            Q.cluster_encode_async(flat, self.clusters, self.block,
+                                   tab_a[to * Q.TABLE_BYTES:(to + u) * Q.TABLE_BYTES],
+                                   lab_a[lo:lo + Q.unit_label_bytes(n, self.block)],
+                                   code_a[co:co + n])
+            quants.append(p)
+        return di
 
     def _finish(self, state):
         """The single synchronisation (every n_c and every cluster table),
