@@ -159,6 +159,29 @@ int bsnp_cluster_dequantize(const uint8_t* labels, const uint8_t* codes, uint64_
                             uint64_t block, const bsnp_cluster_table* tables, float* out,
                             bsnp_status* status, void* ws, size_t ws_bytes, void* stream);
 
+/* One per-tensor (block 0) quantized state of a restore batch. */
+typedef struct bsnp_dequant_item {
+  const uint8_t* labels;            /* (n + 1) / 2 bytes */
+  const uint8_t* codes;             /* n bytes */
+  const bsnp_cluster_table* table;  /* 16-byte aligned */
+  float* out;                       /* n floats, 4-byte aligned */
+  uint64_t n;
+} bsnp_dequant_item;
+
+/* Elements per CTA of bsnp_cluster_dequantize_batch. */
+#define BSNP_DEQUANT_CHUNK 65536u
+
+/*
+ * The restore loop's per-record dequantize (store.py:458-468 calls
+ * quantizer.dequantize once per optimizer record) for many records in one
+ * launch.  items / first / status live in device memory: first[i] is the
+ * index of item i's first BSNP_DEQUANT_CHUNK chunk, nchunks = first[nitems];
+ * status[i] is item i's bsnp_cluster_dequantize status (zeroed here).
+ */
+int bsnp_cluster_dequantize_batch(const bsnp_dequant_item* items, const uint32_t* first,
+                                  uint32_t nitems, uint32_t nchunks, bsnp_status* status,
+                                  void* stream);
+
 /* ------------------------------------------------------------------------
  * Checkpoint blob assembly
  * ---------------------------------------------------------------------- */

@@ -39,6 +39,7 @@ constexpr int kHeapDepth = 7;        // leaves of a <= kTileMax node lie at dept
 constexpr int kHeap = 1 << (kHeapDepth + 1);
 constexpr uint32_t kSmemFloats = kTileMax + (kTileMax / 128) * 8 + 32;
 constexpr uint32_t kDqChunk = 65536;  // elements per dequantize CTA (one LUT build)
+static_assert(kDqChunk == BSNP_DEQUANT_CHUNK, "header chunk size");
 static_assert(sizeof(bsnp_cluster_table) == 256, "table layout is part of the C-ABI");
 
 // shared-memory layout: 8 floats of padding per 128-float chunk so that the
@@ -833,30 +834,15 @@ __global__ void __launch_bounds__(kQThreads)
 }
 
 // --------------------------------------------------------------- dequantize
-__global__ void __launch_bounds__(kQThreads)
-    dequantize_kernel(const uint8_t* __restrict__ labels, const uint8_t* __restrict__ codes,
-                      QPlan P, const bsnp_cluster_table* __restrict__ tables,
-                      float* __restrict__ out, bsnp_status* __restrict__ st) {
-  __shared__ float lut[16 * 256];
-  __shared__ uint32_t s_maxlab;
-  // chunk -> (unit, element range)
-  const uint64_t cidx = blockIdx.x;
-  const uint64_t full_chunks = (uint64_t)(P.nunits - 1) * P.C_full;
-  uint32_t u;
-  uint64_t c0, len;
-  if (cidx < full_chunks) {
-    u = (uint32_t)(cidx / P.C_full);
-    c0 = (cidx % P.C_full) * kDqChunk;
-    len = P.block;
-  } else {
-    u = P.nunits - 1;
-    c0 = (cidx - full_chunks) * kDqChunk;
-    len = P.last_len;
-  }
-  const uint64_t c1 = c0 + kDqChunk < len ? c0 + kDqChunk : len;
-  const bsnp_cluster_table& tb = tables[u];
+// One CTA's chunk [c0, c1) of a unit: LUT from the unit's table, then
+// out = lut[label][code]; the unit's largest label goes to st.
+__device__ __forceinline__ void dequant_chunk(const uint8_t* __restrict__ ls,
+                                              const uint8_t* __restrict__ cs,
+                                              float* __restrict__ o, uint64_t c0, uint64_t c1,
+                                              const bsnp_cluster_table& tb, bsnp_status* st,
+                                              float* lut, uint32_t* s_maxlab) {
   const uint32_t m = tb.m;
-  if (threadIdx.x == 0) s_maxlab = 0;
+  if (threadIdx.x == 0) *s_maxlab = 0;
   for (uint32_t i = threadIdx.x; i < 16 * 256; i += blockDim.x) {
     const uint32_t c = i >> 8, j = i & 255;
     // restored = (qmap(code) * S + b).astype(float32)   (quantizer.py:199-201)
@@ -865,10 +851,6 @@ __global__ void __launch_bounds__(kQThreads)
                    : 0.0f;
   }
   __syncthreads();
-  const uint64_t ustart = (uint64_t)u * P.block;
-  const uint8_t* cs = codes + ustart;
-  const uint8_t* ls = labels + (uint64_t)u * (P.block / 2);
-  float* o = out + ustart;
   uint32_t maxlab = 0;
   const bool vec = ((((uintptr_t)(cs + c0)) & 7) | (((uintptr_t)(ls + c0 / 2)) & 3) |
                     (((uintptr_t)(o + c0)) & 15)) == 0;
@@ -915,12 +897,64 @@ __global__ void __launch_bounds__(kQThreads)
   // the reference raises with the largest label of the tensor (quantizer.py:196-197)
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) maxlab = max(maxlab, __shfl_xor_sync(kFull, maxlab, d));
-  if ((threadIdx.x & 31) == 0 && maxlab) atomicMax(&s_maxlab, maxlab);
+  if ((threadIdx.x & 31) == 0 && maxlab) atomicMax(s_maxlab, maxlab);
   __syncthreads();
-  if (threadIdx.x == 0 && s_maxlab) {
-    atomicMax((unsigned long long*)&st->count, (unsigned long long)s_maxlab);
-    if (s_maxlab >= m) atomicOr(&st->err_flags, BSNP_ERR_LABEL);
+  if (threadIdx.x == 0 && *s_maxlab) {
+    atomicMax((unsigned long long*)&st->count, (unsigned long long)*s_maxlab);
+    if (*s_maxlab >= m) atomicOr(&st->err_flags, BSNP_ERR_LABEL);
   }
+}
+
+__global__ void __launch_bounds__(kQThreads)
+    dequantize_kernel(const uint8_t* __restrict__ labels, const uint8_t* __restrict__ codes,
+                      QPlan P, const bsnp_cluster_table* __restrict__ tables,
+                      float* __restrict__ out, bsnp_status* __restrict__ st) {
+  __shared__ float lut[16 * 256];
+  __shared__ uint32_t s_maxlab;
+  // chunk -> (unit, element range)
+  const uint64_t cidx = blockIdx.x;
+  const uint64_t full_chunks = (uint64_t)(P.nunits - 1) * P.C_full;
+  uint32_t u;
+  uint64_t c0, len;
+  if (cidx < full_chunks) {
+    u = (uint32_t)(cidx / P.C_full);
+    c0 = (cidx % P.C_full) * kDqChunk;
+    len = P.block;
+  } else {
+    u = P.nunits - 1;
+    c0 = (cidx - full_chunks) * kDqChunk;
+    len = P.last_len;
+  }
+  const uint64_t c1 = c0 + kDqChunk < len ? c0 + kDqChunk : len;
+  const uint64_t ustart = (uint64_t)u * P.block;
+  dequant_chunk(labels + (uint64_t)u * (P.block / 2), codes + ustart, out + ustart, c0, c1,
+                tables[u], st, lut, &s_maxlab);
+}
+
+// many per-tensor records, one launch: CTA -> (item, chunk) through first[]
+__global__ void __launch_bounds__(kQThreads)
+    dequantize_batch_kernel(const bsnp_dequant_item* __restrict__ items,
+                            const uint32_t* __restrict__ first, uint32_t nitems,
+                            bsnp_status* __restrict__ st) {
+  __shared__ float lut[16 * 256];
+  __shared__ uint32_t s_maxlab, s_item;
+  const uint32_t b = blockIdx.x;
+  if (threadIdx.x == 0) {
+    uint32_t lo = 0, hi = nitems;  // largest i with first[i] <= b
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (first[mid] <= b) lo = mid;
+      else hi = mid;
+    }
+    s_item = lo;
+  }
+  __syncthreads();
+  const uint32_t i = s_item;
+  const bsnp_dequant_item it = items[i];
+  const uint64_t c0 = (uint64_t)(b - first[i]) * kDqChunk;
+  if (c0 >= it.n) return;
+  const uint64_t c1 = c0 + kDqChunk < it.n ? c0 + kDqChunk : it.n;
+  dequant_chunk(it.labels, it.codes, it.out, c0, c1, *it.table, st + i, lut, &s_maxlab);
 }
 
 // ------------------------------------------------------- precision report
@@ -1181,6 +1215,20 @@ extern "C" int bsnp_cluster_dequantize(const uint8_t* labels, const uint8_t* cod
   const uint64_t chunks = (uint64_t)(P.nunits - 1) * P.C_full + P.C_last;
   dequantize_kernel<<<(unsigned)chunks, kQThreads, 0, s>>>(labels, codes, P, tables, out, status);
   return launch_status("dequantize_kernel");
+}
+
+extern "C" int bsnp_cluster_dequantize_batch(const bsnp_dequant_item* items,
+                                             const uint32_t* first, uint32_t nitems,
+                                             uint32_t nchunks, bsnp_status* status,
+                                             void* stream) {
+  if (nitems == 0) return BSNP_OK;
+  if (!items || !first || !status) return BSNP_E_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = cuda_status("memset(status)",
+                       cudaMemsetAsync(status, 0, (size_t)nitems * sizeof(bsnp_status), s));
+  if (rc || nchunks == 0) return rc;
+  dequantize_batch_kernel<<<nchunks, kQThreads, 0, s>>>(items, first, nitems, status);
+  return launch_status("dequantize_batch_kernel");
 }
 
 extern "C" int bsnp_precision_report(const float* original, const float* restored, uint64_t n,

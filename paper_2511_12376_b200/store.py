@@ -24,6 +24,7 @@ The file-system lifecycle (tracker, commit, recovery, pruning) is out of scope
 
 from __future__ import annotations
 
+import bisect
 import json
 import os
 import struct
@@ -606,6 +607,7 @@ def sequential_offsets(recs) -> list:
 
 _SEG = np.dtype([("src", "<u8"), ("dst", "<u8"), ("len", "<u8")])  # bsnp_segment
 GATHER_CHUNK = 65536                                                  # BSNP_GATHER_CHUNK
+DEQUANT_CHUNK = 65536                                                 # BSNP_DEQUANT_CHUNK
 GATHER_MIN_AVG = 4 << 20  # average record bytes above which records are copied one by one
 GRAPH_MAX_ARENA = 4 << 30  # arena bytes above which encode_records does not record a graph
 
@@ -805,6 +807,10 @@ def decode_chain(chain, device: torch.device | None = None, to_host: bool = True
             meta[t.name] = (t.dtype, tuple(t.shape))
             model_order.append(t.name)
     with torch.cuda.device(dev):
+        # every link's upload is queued up front on the copy stream, so the
+        # PCIe stream never idles between links; the device checks of all
+        # links come back in one read at the end
+        links = []
         for ci, (manifest, blob) in enumerate(chain):
             # only the final checkpoint's optimizer states are restored: an
             # earlier link needs just the span of its model records
@@ -822,66 +828,23 @@ def decode_chain(chain, device: torch.device | None = None, to_host: bool = True
                 pin.numpy()[:k] = np.frombuffer(mv[:k], dtype=np.uint8)
             need = len(mv) if need is None else min(need, len(mv))
             dblob = torch.empty(need, dtype=torch.uint8, device=dev)
-            ready = _ChunkedUpload(pin, dblob, need, dev)
-            if manifest.kind == KIND_BASE:
-                model_order = []
-            checks = []
-            nd = sum(1 for e in manifest.tensors
-                     if e.group == GROUP_MODEL and e.codec != CODEC_RAW)
-            sts = rt.new_status(dev, max(nd, 1))  # one status block per delta, one read
-            for e in manifest.tensors:
-                if e.group != GROUP_MODEL:
-                    continue
-                ready(e.offset + e.length)
-                if e.codec == CODEC_RAW:
-                    name, dtype, shape, bo, k = _parse_raw(mv, e.offset)
-                    dt = torch.int16 if dtype is ElementType.F16 else torch.float32
-                    model[name] = dblob[bo:bo + k].clone().view(dt)
-                    meta[name] = (dtype, shape)
-                else:
-                    name, shape, n, n_c, mo, po = _parse_delta(mv, e.offset)
-                    if name not in model:
-                        raise KeyError(name)
-                    if meta[name][1] != shape:
-                        raise B.DeltaError(f"shape mismatch for {name!r}: "
-                                           f"{meta[name][1]} vs {shape}")
-                    base = model[name]
-                    if base.numel() != n:
-                        raise B.DeltaError("element count mismatch")
-                    if base.dtype != torch.int16:
-                        raise B.DeltaError("delta encoding requires F16 tensors")
-                    st = sts[len(checks)]
-                    if n:
-                        pay = dblob[po:po + 2 * n_c]
-                        if po & 1:
-                            pay = pay.clone()
-                        B.decode_delta_async(base, dblob[mo:mo + (n + 7) // 8],
-                                             pay.view(torch.int16), n_c, base, st)
-                    else:
-                        st.zero_()
-                    checks.append(n_c)
-                    meta[name] = (ElementType.F16, shape)
+            links.append((manifest, mv, dblob, _ChunkedUpload(pin, dblob, need, dev)))
+        checks = []        # deferred device checks, in the reference's raise order
+        try:
+            for ci, (manifest, mv, dblob, ready) in enumerate(links):
+                final = ci == len(links) - 1
+                plan = _LinkPlan(manifest, mv, ready, final)
                 if manifest.kind == KIND_BASE:
-                    model_order.append(e.name)
-            if checks:
-                for (pc, flags), n_c in zip(rt.read_status(sts[:len(checks)]), checks):
-                    B._raise_decode_flags(flags, pc, n_c)
-            if ci < len(chain) - 1:
+                    model_order = [e.name for e in manifest.tensors if e.group == GROUP_MODEL]
+                plan.check_deltas(model, meta)
+                opt = plan.launch(dev, dblob, model, meta, checks)
+                if final:
+                    final_opt = opt
                 ready.finish()
-            if ci == len(chain) - 1:
-                opt = [e for e in manifest.tensors if e.group == GROUP_OPTIMIZER]
-                deq = iter(_dequant_entries(mv, dblob,
-                                            [e for e in opt if e.codec == CODEC_QUANT], dev,
-                                            ready))
-                for e in opt:
-                    if e.codec == CODEC_QUANT:
-                        final_opt.append(next(deq))
-                    else:
-                        ready(e.offset + e.length)
-                        name, dtype, shape, bo, k = _parse_raw(mv, e.offset)
-                        dt = torch.int16 if dtype is ElementType.F16 else torch.float32
-                        final_opt.append((name, dtype, shape, dblob[bo:bo + k].clone().view(dt)))
-                ready.finish()
+        except Exception:
+            _run_checks(checks)  # an earlier link's device error is reported first
+            raise
+        _run_checks(checks)
         if not model_order:
             model_order = list(model)
         final = chain[-1][0]
@@ -920,7 +883,12 @@ class _ChunkedUpload:
                 self.bounds.append(b)
         dblob.record_stream(cs)
 
-    def __call__(self, end: int) -> None:
+    def __call__(self, end: int, stream=None) -> None:
+        if stream is not None:  # a side stream: wait for the chunk holding `end`
+            if self.bounds:
+                i = min(bisect.bisect_left(self.bounds, end), len(self.bounds) - 1)
+                stream.wait_event(self.events[i])
+            return
         if self.waited >= 0 and self.bounds[self.waited] >= end:
             return
         for i in range(self.waited + 1, len(self.bounds)):
@@ -929,6 +897,12 @@ class _ChunkedUpload:
             if self.bounds[i] >= end:
                 break
 
+    def chunk_of(self, end: int) -> int:
+        """Index of the chunk holding byte end-1 (0 when nothing uploads)."""
+        if not self.bounds:
+            return 0
+        return min(bisect.bisect_left(self.bounds, end), len(self.bounds) - 1)
+
     def finish(self) -> None:
         """The current stream waits for every chunk."""
         if self.bounds:
@@ -936,6 +910,31 @@ class _ChunkedUpload:
 
 
 _COPY_STREAMS: dict = {}
+_SIDE_STREAMS: dict = {}
+
+
+class _Lanes:
+    """Independent per-tensor launches round-robin over side streams forked
+    from the current stream; join() makes the current stream wait for all."""
+
+    def __init__(self, dev, k: int = 8):
+        self.main = torch.cuda.current_stream(dev)
+        key = torch.device(dev).index
+        if key not in _SIDE_STREAMS:
+            _SIDE_STREAMS[key] = [torch.cuda.Stream(torch.device(dev)) for _ in range(k)]
+        self.side = _SIDE_STREAMS[key]
+        for ss in self.side:
+            ss.wait_stream(self.main)
+        self.i = 0
+
+    def next(self):
+        ss = self.side[self.i % len(self.side)]
+        self.i += 1
+        return ss
+
+    def join(self) -> None:
+        for ss in self.side:
+            self.main.wait_stream(ss)
 
 
 def _copy_stream(dev) -> torch.cuda.Stream:
@@ -945,50 +944,244 @@ def _copy_stream(dev) -> torch.cuda.Stream:
     return _COPY_STREAMS[key]
 
 
-def _dequant_entries(mv: memoryview, dblob: torch.Tensor, entries, dev, ready=None) -> list:
-    """BSQT records -> dequantized device tensors.  Labels and codes are read
-    in place from the device copy of the blob; every table goes up in one
-    copy and every status comes back in one read."""
-    parsed, tabs = [], bytearray()
-    for e in entries:
-        cur = ByteCursor(mv[e.offset:e.offset + e.length])
-        cur.magic(Q.QUANT_MAGIC)
-        (ver,) = cur.unpack("<H")
-        if ver != Q.QUANT_VERSION:
-            raise Q.QuantizerError(f"unsupported quantized-tensor version {ver}")
-        (m,) = cur.unpack("<B")
-        mean, std = cur.unpack("<ff")
-        table = Q.ClusterTable(m=m, mean=mean, std=std, boundaries=cur.unpack(f"<{m - 1}f"),
-                               scales=cur.unpack(f"<{m}f"), offsets=cur.unpack(f"<{m}f"))
-        name, shape = cur.name_and_shape()
-        n = 1
-        for d in shape:
-            n *= d
-        lo = e.offset + cur.pos
-        cur.take((n + 1) // 2)
-        co = e.offset + cur.pos
-        cur.take(n)
-        parsed.append((name, shape, n, m, lo, co, len(tabs)))
-        tabs += table.to_device_bytes()
-    if not parsed:
-        return []
-    dtabs = rt.h2d_bytes(bytes(tabs), dev)
-    sts = rt.new_status(dev, len(parsed))
-    outs = []
-    for i, (name, shape, n, m, lo, co, to) in enumerate(parsed):
-        out = torch.empty(n, dtype=torch.float32, device=dev)
-        if ready is not None:
-            ready(co + n)
-        if n:
-            Q.cluster_dequantize_async(dblob[lo:lo + (n + 1) // 2], dblob[co:co + n], n, 0,
-                                       dtabs[to:to + Q.TABLE_BYTES], out, sts[i])
-        else:
-            sts[i].zero_()
-        outs.append((name, ElementType.F32, shape, out))
-    for (maxlab, flags), (_, _, _, m, _, _, _) in zip(rt.read_status(sts), parsed):
-        if flags & _lib.ERR_LABEL:
-            raise Q.QuantizerError(f"label {maxlab} >= m={m}")
-    return outs
+_DQI = np.dtype([("labels", "<u8"), ("codes", "<u8"), ("table", "<u8"), ("out", "<u8"),
+                 ("n", "<u8")])                                                 # bsnp_dequant_item
+
+
+def _align(x: int, a: int) -> int:
+    return (x + a - 1) // a * a
+
+
+def _run_checks(checks) -> None:
+    """Device status checks deferred to the end of a restore: one read of
+    each status tensor, errors raised in the order they were queued."""
+    cache = {}
+    for st, fn in checks:
+        key = id(st)
+        if key not in cache:
+            cache[key] = (st, rt.read_status(st))
+        fn(cache[key][1])
+
+
+class _LinkPlan:
+    """One chain link's records grouped by the upload chunk that completes
+    them (store.py:429-474 replays them one by one).  Per chunk: one gather
+    launch for the RAW records (into an aligned arena; odd-offset delta
+    payloads are realigned by the same launch), one batched dequantize for
+    the quantized optimizer records, and the in-place delta decodes."""
+
+    def __init__(self, manifest, mv, ready, final: bool):
+        self.raws, self.deltas, self.quants = [], [], []
+        for e in manifest.tensors:
+            if e.group == GROUP_MODEL:
+                if e.codec == CODEC_RAW:
+                    name, dtype, shape, bo, k = _parse_raw(mv, e.offset)
+                    self.raws.append((ready.chunk_of(e.offset + e.length), e.group, name, dtype,
+                                      shape, bo, k))
+                else:
+                    name, shape, n, n_c, mo, po = _parse_delta(mv, e.offset)
+                    self.deltas.append((ready.chunk_of(e.offset + e.length), name, shape, n,
+                                        n_c, mo, po))
+            elif final:
+                if e.codec == CODEC_QUANT:
+                    self.quants.append((ready.chunk_of(e.offset + e.length),)
+                                       + _parse_quant(mv, e))
+                else:
+                    name, dtype, shape, bo, k = _parse_raw(mv, e.offset)
+                    self.raws.append((ready.chunk_of(e.offset + e.length), e.group, name, dtype,
+                                      shape, bo, k))
+        self.final = final
+        self.ready = ready
+        self.order = [(e.group, e.codec, e.name) for e in manifest.tensors
+                      if final or e.group == GROUP_MODEL]
+
+    def check_deltas(self, model, meta) -> None:
+        """The host-side checks of decode_delta (bitmask.py:114-127), in order."""
+        for _, name, shape, n, n_c, mo, po in self.deltas:
+            if name not in model:
+                raise KeyError(name)
+            if meta[name][1] != shape:
+                raise B.DeltaError(f"shape mismatch for {name!r}: {meta[name][1]} vs {shape}")
+            base = model[name]
+            if base.numel() != n:
+                raise B.DeltaError("element count mismatch")
+            if base.dtype != torch.int16:
+                raise B.DeltaError("delta encoding requires F16 tensors")
+
+    def launch(self, dev, dblob, model, meta, checks) -> list:
+        """Queues the link; returns the final link's optimizer states."""
+        lib = rt.lib()
+        nchunk = max(len(self.ready.bounds), 1)
+        # arenas: RAW records and realigned payloads (bytes), dequantized f32
+        raw_off, ra = [], 0
+        for r in self.raws:
+            raw_off.append(ra)
+            ra = _align(ra + r[6], 256)
+        pay_off = {}
+        for i, d in enumerate(self.deltas):
+            if d[3] and d[6] & 1:
+                pay_off[i] = ra
+                ra = _align(ra + 2 * d[4], 256)
+        q_off, qa = [], 0
+        for q in self.quants:
+            q_off.append(qa)
+            qa = _align(qa + q[3], 64)
+        arena = torch.empty(max(ra, 1), dtype=torch.uint8, device=dev)
+        qarena = torch.empty(max(qa, 1), dtype=torch.float32, device=dev)
+        nd, nq = len(self.deltas), len(self.quants)
+        sts = rt.new_status(dev, max(nd + nq, 1))
+        # per chunk: segments, items; one metadata upload for the link
+        seg_g = [[] for _ in range(nchunk)]
+        for i, r in enumerate(self.raws):
+            seg_g[r[0]].append((dblob.data_ptr() + r[5], raw_off[i], r[6]))
+        for i, off in pay_off.items():
+            d = self.deltas[i]
+            seg_g[d[0]].append((dblob.data_ptr() + d[6], off, 2 * d[4]))
+        q_g = [[] for _ in range(nchunk)]
+        for i, q in enumerate(self.quants):
+            q_g[q[0]].append(i)
+        tab_at = 0
+        layout, cur = [], _align(nq * Q.TABLE_BYTES, 16)
+        for g in range(nchunk):
+            ns, ni = len(seg_g[g]), len(q_g[g])
+            so = cur
+            cur = _align(so + _SEG.itemsize * ns, 8)
+            sf = cur
+            cur = _align(sf + 4 * (ns + 1), 8)
+            io = cur
+            cur = _align(io + _DQI.itemsize * ni, 8)
+            fi = cur
+            cur = _align(fi + 4 * (ni + 1), 16)
+            layout.append((so, sf, io, fi))
+        host = torch.empty(max(cur, 1), dtype=torch.uint8, pin_memory=True)
+        hb = host.numpy()
+        mdev = torch.empty(max(cur, 1), dtype=torch.uint8, device=dev)
+        mbase, qbase, sbase = mdev.data_ptr(), qarena.data_ptr(), sts.data_ptr()
+        for i, q in enumerate(self.quants):
+            hb[tab_at + i * Q.TABLE_BYTES:tab_at + (i + 1) * Q.TABLE_BYTES] = \
+                np.frombuffer(q[6], dtype=np.uint8)
+        launches = []
+        cw = GATHER_CHUNK
+        qc = DEQUANT_CHUNK
+        for g in range(nchunk):
+            so, sf, io, fi = layout[g]
+            segs = seg_g[g]
+            if segs:
+                arr = np.array(segs, dtype=np.uint64)
+                hb[so:so + _SEG.itemsize * len(segs)] = arr.view(np.uint8).reshape(-1)
+                fst = np.zeros(len(segs) + 1, dtype=np.uint32)
+                np.cumsum((arr[:, 2] + cw - 1) // cw, out=fst[1:])
+                hb[sf:sf + 4 * len(fst)] = fst.view(np.uint8)
+                segs = (mbase + so, mbase + sf, len(segs), int(fst[-1]))
+            items = q_g[g]
+            if items:
+                it = np.zeros(len(items), dtype=_DQI)
+                fst = np.zeros(len(items) + 1, dtype=np.uint32)
+                for j, i in enumerate(items):
+                    q = self.quants[i]
+                    it[j] = (dblob.data_ptr() + q[4], dblob.data_ptr() + q[5],
+                             mbase + tab_at + i * Q.TABLE_BYTES, qbase + 4 * q_off[i], q[3])
+                    fst[j + 1] = fst[j] + (q[3] + qc - 1) // qc
+                hb[io:io + _DQI.itemsize * len(items)] = it.view(np.uint8)
+                hb[fi:fi + 4 * len(fst)] = fst.view(np.uint8)
+                # consecutive status rows: the batch zeroes and fills them
+                items = (mbase + io, mbase + fi, len(items), int(fst[-1]),
+                         sbase + 16 * (nd + items[0]))
+            launches.append((segs, items))
+        mdev.copy_(host, non_blocking=True)
+        lanes = _Lanes(dev)
+        # the delta decodes go round-robin over the lanes; a chunk's gather
+        # runs first on its own lane (realigned payloads), so deltas needing
+        # it follow on that lane
+        dec_ws = lib.bsnp_delta_decode_ws_bytes
+        ws = {}
+        for ss in lanes.side:
+            need = max((dec_ws(d[3]) for d in self.deltas), default=0)
+            with torch.cuda.stream(ss):
+                ws[ss] = rt.workspace(dev, max(need, 1), "dec")
+        glane = []
+        for g in range(nchunk):
+            segs, items = launches[g]
+            lane = lanes.next()
+            glane.append(lane)
+            if not (segs or items):
+                continue
+            self.ready(self.ready.bounds[g] if self.ready.bounds else 0, lane)
+            sp = lane.cuda_stream
+            if segs:
+                _lib.check(lib.bsnp_gather_segments(segs[0], segs[1], segs[2], segs[3],
+                                                    arena.data_ptr(), sp), "bsnp_gather_segments")
+            if items:
+                _lib.check(lib.bsnp_cluster_dequantize_batch(items[0], items[1], items[2],
+                                                             items[3], items[4], sp),
+                           "bsnp_cluster_dequantize_batch")
+        # the RAW records become the tensors (views of the arena)
+        opt = {}
+        for i, (g, group, name, dtype, shape, bo, k) in enumerate(self.raws):
+            dt = torch.int16 if dtype is ElementType.F16 else torch.float32
+            t = arena[raw_off[i]:raw_off[i] + k].view(dt)
+            if group == GROUP_MODEL:
+                model[name] = t
+                meta[name] = (dtype, shape)
+            else:
+                opt[name] = (name, dtype, shape, t)
+        for i, (g, name, shape, n, n_c, mo, po) in enumerate(self.deltas):
+            st = sbase + 16 * i
+            if i in pay_off:
+                lane = glane[g]
+                pay = arena.data_ptr() + pay_off[i]
+            else:
+                lane = lanes.next()
+                self.ready(self.ready.bounds[g] if self.ready.bounds else 0, lane)
+                pay = dblob.data_ptr() + po
+            base = model[name].data_ptr()
+            w = ws[lane]
+            _lib.check(lib.bsnp_delta_decode(base, dblob.data_ptr() + mo if n else None,
+                                             pay if n_c else None, n, n_c, base if n else None,
+                                             st, w.data_ptr(), w.numel(), lane.cuda_stream),
+                       "bsnp_delta_decode")
+            meta[name] = (ElementType.F16, shape)
+        lanes.join()
+        ndl = [d[4] for d in self.deltas]
+        if nd:
+            checks.append((sts, lambda res, ndl=ndl: [B._raise_decode_flags(f, pc, c)
+                                                     for (pc, f), c in zip(res[:len(ndl)], ndl)]))
+        if nq:
+            ms = [q[7] for q in self.quants]
+
+            def qcheck(res, ms=ms, nd=nd):
+                for (maxlab, flags), m in zip(res[nd:nd + len(ms)], ms):
+                    if flags & _lib.ERR_LABEL:
+                        raise Q.QuantizerError(f"label {maxlab} >= m={m}")
+            checks.append((sts, qcheck))
+        if not self.final:
+            return []
+        for i, q in enumerate(self.quants):
+            opt[q[1]] = (q[1], ElementType.F32, q[2], qarena[q_off[i]:q_off[i] + q[3]])
+        return [opt[name] for group, codec, name in self.order if group == GROUP_OPTIMIZER]
+
+
+def _parse_quant(mv: memoryview, e):
+    """A BSQT record -> (name, shape, n, labels offset, codes offset,
+    device table bytes, m)."""
+    cur = ByteCursor(mv[e.offset:e.offset + e.length])
+    cur.magic(Q.QUANT_MAGIC)
+    (ver,) = cur.unpack("<H")
+    if ver != Q.QUANT_VERSION:
+        raise Q.QuantizerError(f"unsupported quantized-tensor version {ver}")
+    (m,) = cur.unpack("<B")
+    mean, std = cur.unpack("<ff")
+    table = Q.ClusterTable(m=m, mean=mean, std=std, boundaries=cur.unpack(f"<{m - 1}f"),
+                           scales=cur.unpack(f"<{m}f"), offsets=cur.unpack(f"<{m}f"))
+    name, shape = cur.name_and_shape()
+    n = 1
+    for d in shape:
+        n *= d
+    lo = e.offset + cur.pos
+    cur.take((n + 1) // 2)
+    co = e.offset + cur.pos
+    cur.take(n)
+    return name, shape, n, lo, co, table.to_device_bytes(), m
 
 
 def write_tensors_bin(path: str, blob) -> None:

@@ -136,6 +136,13 @@ def test_random_chain_vs_oracle(dev, clusters):
     rec = S.decode_chain(chain)
     for a, b in zip(rec.model_states, c2.model_states):
         assert a.data == b.data
+    # the batched dequantize (one launch per upload chunk) vs the oracle
+    assert [t.name for t in rec.optimizer_states] == [t.name for t in c2.optimizer_states]
+    for a, b in zip(rec.optimizer_states, c2.optimizer_states):
+        x = np.frombuffer(b.data, np.float32)
+        tab = O.cluster_fit(x, clusters)
+        p, c, _ = O.cluster_quantize(x, tab)
+        assert a.data == O.cluster_dequantize(p, c, x.size, tab).astype("<f4").tobytes()
 
 
 def test_store_errors(dev):
@@ -161,6 +168,22 @@ def test_store_errors(dev):
     from paper_2511_12376_b200.bitmask import DeltaError
     with pytest.raises(DeltaError, match="padding"):
         S.decode_chain([(man0, b0), (man1, bytes(bad))])
+    # a label >= m in a quantized record (quantizer.py:196-197) is rejected
+    man5, b5 = S.encode_checkpoint(c1, c0, S.KIND_DELTA, clusters=5)
+    e = [x for x in man5.tensors if x.codec == "QUANT"][2]
+    lo = S._parse_quant(memoryview(b5), e)[3]
+    bad = bytearray(b5)
+    bad[lo] = 0xF7
+    from paper_2511_12376_b200.quantizer import QuantizerError
+    with pytest.raises(QuantizerError, match="label 15 >= m=5"):
+        S.decode_chain([(man0, b0), (man5, bytes(bad))])
+    # the delta error of the same restore is reported first (model records
+    # are replayed before the optimizer records)
+    bad2 = bytearray(bad)
+    e = [x for x in man5.tensors if x.codec == "DELTA" and x.name == "p6"][0]
+    bad2[e.offset + hdr + (n + 7) // 8 - 1] |= 0x80
+    with pytest.raises(DeltaError, match="padding"):
+        S.decode_chain([(man0, b0), (man5, bytes(bad2))])
 
 
 def test_planner_world1_with_gpu_encoder(dev, tmp_path):
