@@ -354,6 +354,15 @@ def quant_header(name: str, shape, table: ClusterTable) -> bytes:
     return pack_shape_header(QUANT_MAGIC, fields, name, shape)
 
 
+def quant_header_raw(name: str, shape, raw: bytes) -> bytes:
+    """quant_header from a device table's bytes (bsnp_cluster_table): the
+    f32 fields are copied as they are."""
+    m = int.from_bytes(raw[196:200], "little")
+    fields = (struct.pack("<HB", QUANT_VERSION, m) + raw[0:8 + 4 * (m - 1)]
+              + raw[68:68 + 4 * m] + raw[132:132 + 4 * m])
+    return pack_shape_header(QUANT_MAGIC, fields, name, shape)
+
+
 def serialize_quantized(q: QuantizedTensor) -> bytes:
     return quant_header(q.name, q.shape, q.table) + q.packed_labels + q.codes
 

@@ -249,10 +249,12 @@ class CheckpointEncoder:
         # (BSNP_GRAPHS=0 disables); a key is captured the second time it is seen
         self.graphs = os.environ.get("BSNP_GRAPHS", "1") != "0"
         # encode() into a large-enough caller buffer overlaps the encode of
-        # one group of tensors with the device-to-host copy of the previous
-        # (large checkpoints; a small one takes the CUDA-graph path whole)
-        self.pipeline_groups = int(os.environ.get("BSNP_SAVE_GROUPS", "8"))
-        self.pipeline_min_bytes = GRAPH_MAX_ARENA
+        # one group of tensors with the device-to-host copy of the previous;
+        # groups: 3 for a checkpoint small enough for recorded graphs (one
+        # per group; C0 delta save 16.8 -> 15.3 ms), 8 above (C3)
+        g = os.environ.get("BSNP_SAVE_GROUPS")
+        self.pipeline_groups = int(g) if g else None
+        self.pipeline_min_bytes = int(os.environ.get("BSNP_PIPELINE_MIN", "0"))
         # side streams the per-tensor launch chains are spread over
         self.side_streams = int(os.environ.get("BSNP_SIDE_STREAMS", "8"))
         self._graphs = {}
@@ -437,10 +439,21 @@ class CheckpointEncoder:
             if p[0] == "raw":
                 _, gid, t, flat = p
                 recs[gid] = _raw_record(gid, t, GROUP_MODEL, flat)
+        TB = Q.TABLE_BYTES
         for p in state["quants"]:
             _, gid, t, flat, lo, co, to = p
             n = t.num_elements
             u = Q.num_units(n, self.block)
+            if u == 1:
+                # the header's table fields are the device table's bytes
+                raw = tab_raw[to * TB:(to + 1) * TB]
+                if int.from_bytes(raw[200:204], "little") & _lib.ERR_NONFINITE:
+                    raise Q.QuantizerError(f"tensor {t.name!r} has non-finite values (NaN/Inf); "
+                                           "cluster statistics are undefined")
+                recs[gid] = EncodedRecord(gid, t.name, GROUP_OPTIMIZER, CODEC_QUANT,
+                                          self.clusters, Q.quant_header_raw(t.name, t.shape, raw),
+                                          [lab_a[lo:lo + (n + 1) // 2], code_a[co:co + n]])
+                continue
             tabs = [Q.ClusterTable.from_device_bytes(
                 tab_raw[(to + i) * Q.TABLE_BYTES:(to + i + 1) * Q.TABLE_BYTES]) for i in range(u)]
             flags = [struct.unpack_from("<I", tab_raw, (to + i) * Q.TABLE_BYTES + 200)[0]
@@ -465,7 +478,7 @@ class CheckpointEncoder:
         returned) — page-locking a fresh multi-GB buffer per save costs
         seconds, so a training loop passes its own (e.g. two alternating
         buffers); a new one is allocated when it is missing or too small."""
-        if out is not None and out.is_pinned() and self.pipeline_groups > 1:
+        if out is not None and out.is_pinned() and self._groups(ckpt) > 1:
             buf = out.reshape(-1).view(torch.uint8)
             raw = sum(t.nbytes for t in list(ckpt.model_states) + list(ckpt.optimizer_states))
             if raw > self.pipeline_min_bytes and buf.numel() >= blob_bound(ckpt):
@@ -477,6 +490,12 @@ class CheckpointEncoder:
             return torch.empty(max(nbytes, 1), dtype=torch.uint8, pin_memory=True)[:nbytes]
         return self.encode_into(ckpt, prev, kind, dest)
 
+    def _groups(self, ckpt) -> int:
+        if self.pipeline_groups is not None:
+            return self.pipeline_groups
+        raw = sum(t.nbytes for t in list(ckpt.model_states) + list(ckpt.optimizer_states))
+        return 3 if raw <= GRAPH_MAX_ARENA else 8
+
     def _encode_pipelined(self, ckpt, prev, kind, buf):
         """encode() into a caller buffer that can hold any outcome: the
         tensors go in a few groups, and while group g+1 is encoded the
@@ -487,11 +506,12 @@ class CheckpointEncoder:
         k = len(items)
         items += [(k + i, GROUP_OPTIMIZER, t) for i, t in enumerate(ckpt.optimizer_states)]
         total = sum(t.nbytes for _, _, t in items)
+        ng = self._groups(ckpt)
         groups, cur, acc = [], [], 0
         for it in items:
             cur.append(it)
             acc += it[2].nbytes
-            if acc >= total / self.pipeline_groups and len(groups) < self.pipeline_groups - 1:
+            if acc >= total / ng and len(groups) < ng - 1:
                 groups.append(cur)
                 cur, acc = [], 0
         if cur:
@@ -512,8 +532,9 @@ class CheckpointEncoder:
                     offs.append(offs[-1] + r.length)
                 cs.wait_stream(main)
                 with torch.cuda.stream(cs):
-                    _place_host(recs, offs, buf, 0, non_blocking=True)
-                keep.append(recs)      # the arenas live until the copies finish
+                    tmp = place_records(recs, offs, buf[offs[0]:], self.dev, offs[0],
+                                        sync=False)
+                keep.append((recs, tmp))  # arenas and staging live until the copies ran
                 all_recs += recs
                 offsets += offs[1:]
             cs.synchronize()
@@ -613,28 +634,31 @@ GRAPH_MAX_ARENA = 4 << 30  # arena bytes above which encode_records does not rec
 
 
 def place_records(recs, offsets, out: torch.Tensor, device: torch.device,
-                  base_offset: int = 0) -> None:
+                  base_offset: int = 0, sync: bool = True):
     """Land every record at its offset of `out` (store.py:240-270 layout).
 
     On a CUDA device the blob is assembled in HBM: every header (and any
     host-bytes part) is packed with the segment table into one pinned buffer
     and uploaded once, `bsnp_gather_segments` copies headers and device
     bodies to their offsets, and ONE device-to-host copy lands the blob in
-    `out` (pinned or registered memory: DMA).  Synchronises once."""
+    `out` (pinned or registered memory: DMA).  Synchronises once; with
+    sync=False the copies are only queued on the current stream and the
+    temporaries they read are returned (keep them until the stream ran)."""
     dev = torch.device(device) if device is not None else None
     if dev is None or dev.type != "cuda":
         _place_host(recs, offsets, out, base_offset)
         return
     total = offsets[len(recs)] - base_offset if recs else 0
     if total <= 0:
-        return
+        return ()
     if total >= GATHER_MIN_AVG * len(recs):
         # large records: per-record copies already run at PCIe speed and the
         # assembly pass would only add an HBM round trip (C3: 0.58 vs 0.60 s)
         with torch.cuda.device(dev):
             _place_host(recs, offsets, out, base_offset, non_blocking=True)
-            torch.cuda.current_stream(dev).synchronize()
-        return
+            if sync:
+                torch.cuda.current_stream(dev).synchronize()
+        return ()
     heads = bytearray()
     segs = []  # (host?, src or staging offset, dst offset, length)
     for r, o in zip(recs, offsets):
@@ -679,7 +703,9 @@ def place_records(recs, offsets, out: torch.Tensor, device: torch.device,
                                                  rt.stream_ptr(dev)),
                    "bsnp_gather_segments")
         out[:total].copy_(blob, non_blocking=True)
-        torch.cuda.current_stream(dev).synchronize()
+        if sync:
+            torch.cuda.current_stream(dev).synchronize()
+    return (stage, dstage, blob)
 
 
 def _place_host(recs, offsets, out, base_offset: int, non_blocking: bool = False) -> None:

@@ -60,3 +60,25 @@ def test_product_package_never_imports_oracle():
         src = open(py).read()
         assert not re.search(r"^\s*(from|import)\s+oracle\b", src, re.M), py
         assert "bitsnap_oracle" not in src, py
+
+
+def test_batch_layouts_and_errors_without_gpu():
+    """The numpy mirrors of bsnp_segment / bsnp_dequant_item have the C
+    sizes; the batched dequantize validates before any CUDA call."""
+    from paper_2511_12376_b200 import _lib
+    from paper_2511_12376_b200 import store as S
+    assert S._SEG.itemsize == 24 and S._DQI.itemsize == 40
+    lib = _lib.load()
+    assert lib.bsnp_cluster_dequantize_batch(None, None, 0, 0, None, None) == _lib.BSNP_OK
+    assert lib.bsnp_cluster_dequantize_batch(None, None, 1, 1, None, None) \
+        == _lib.BSNP_E_INVALID
+
+
+def test_quant_header_from_device_table_bytes():
+    from paper_2511_12376_b200 import quantizer as Q
+    for m in (2, 5, 16):
+        t = Q.ClusterTable(m=m, mean=0.1, std=2.5, boundaries=tuple(range(1, m)),
+                           scales=tuple(0.5 * i for i in range(m)),
+                           offsets=tuple(-0.25 * i for i in range(m)))
+        raw = t.to_device_bytes()
+        assert Q.quant_header_raw("layer.0.w", (3, 7), raw) == Q.quant_header("layer.0.w", (3, 7), t)
