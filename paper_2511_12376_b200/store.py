@@ -592,12 +592,16 @@ class CheckpointEncoder:
 
 def blob_bound(ckpt: Checkpoint) -> int:
     """An upper bound of the tensors.bin size of any encoding of `ckpt`: a
-    DELTA record is chosen only when smaller than the RAW one, and a BSQT
-    record (1.5 bytes per element plus a header) is smaller than the f32 RAW
-    record plus its 256-byte allowance."""
+    DELTA record is chosen only when smaller than the RAW one, and an F32
+    optimizer state is always a BSQT record (store.py:261-263): 1.5 bytes
+    per element plus a header at most 256 bytes longer than the RAW one."""
     b = 0
-    for t in list(ckpt.model_states) + list(ckpt.optimizer_states):
+    for t in ckpt.model_states:
         b += len(tensor_header(t.name, t.dtype, t.shape)) + t.nbytes + 256
+    for t in ckpt.optimizer_states:
+        n = t.num_elements
+        body = (n + 1) // 2 + n if t.dtype is ElementType.F32 else t.nbytes
+        b += len(tensor_header(t.name, t.dtype, t.shape)) + body + 256
     return b
 
 
@@ -867,6 +871,9 @@ def decode_chain(chain, device: torch.device | None = None, to_host: bool = True
                 if final:
                     final_opt = opt
                 ready.finish()
+                # the link's device blob returns to the allocator (its reads
+                # are ordered before anything the current stream queues next)
+                links[ci] = dblob = None
         except Exception:
             _run_checks(checks)  # an earlier link's device error is reported first
             raise

@@ -102,6 +102,21 @@ def test_staging_blob_matches_reference(eg, checkpoint_golden, tmp_path):
         S.unpack_blob(b"NOPE" + blob[4:])
 
 
+def test_blob_bound_covers_reference_blobs(checkpoint_golden, golden_index):
+    """store.blob_bound (the caller-buffer size of a pipelined save) is an
+    upper bound of the reference's base and delta blobs of the golden
+    checkpoint, and tight for the quantized optimizer records."""
+    from test_store_gpu import _golden_ckpts
+    g = checkpoint_golden
+    c0, c1 = _golden_ckpts(g, golden_index["checkpoint"])
+    for ck, blob in ((c0, g["blob0"]), (c1, g["blob1"])):
+        bound = S.blob_bound(ck)
+        assert blob.size <= bound
+        opt = sum(t.num_elements for t in ck.optimizer_states)
+        assert bound < sum(t.nbytes for t in ck.model_states) + 1.5 * opt + 600 * (
+            len(ck.model_states) + len(ck.optimizer_states))
+
+
 def _consensus_region(path):
     region = E.SlotRegion.create(path, ranks=2, redundancy=3, capacity=16)
     region.stage(0, b"r0-it3", 3)

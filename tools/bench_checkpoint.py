@@ -52,16 +52,42 @@ def shapes(config: str):
             out += [(p + "gate", (ffn, d)), (p + "up", (ffn, d)), (p + "down", (d, ffn)),
                     (p + "in_norm", (d,)), (p + "post_norm", (d,))]
         return out
+    if config == "C4":   # Llama-2-70B: GQA k/v (1024, 8192), ffn 28672
+        d, ffn, kv, vocab, layers = 8192, 28672, 1024, 32000, 80
+        out = [("embed", (vocab, d)), ("lm_head", (vocab, d)), ("norm", (d,))]
+        for i in range(layers):
+            p = f"layers.{i}."
+            out += [(p + "q", (d, d)), (p + "k", (kv, d)), (p + "v", (kv, d)), (p + "o", (d, d)),
+                    (p + "gate", (ffn, d)), (p + "up", (ffn, d)), (p + "down", (d, ffn)),
+                    (p + "in_norm", (d,)), (p + "post_norm", (d,))]
+        return out
     raise ValueError(config)
 
 
-def generate(config: str, dev, seed: int = 0):
+def shard_names(config: str, rank: int, world: int):
+    """The tensors planner.plan_shards gives `rank` of `world` (LPT over the
+    bf16 w + base + fp32 m, v bytes of each tensor)."""
+    from paper_2511_12376_b200.planner import plan_shards
+    shp = shapes(config)
+    raw = []
+    for _, s in shp:
+        n = 1
+        for x in s:
+            n *= x
+        raw.append(12 * n)
+    plan = plan_shards(raw, world)
+    return {name for (name, _), r in zip(shp, plan.owner) if r == rank}, plan
+
+
+def generate(config: str, dev, seed: int = 0, only=None):
     import torch
     from paper_2511_12376_b200.store import DeviceTensor
     from paper_2511_12376_b200.tensors import Checkpoint
     g = torch.Generator(device=dev).manual_seed(seed)
     base, cur, opt = [], [], []
     for name, shp in shapes(config):
+        if only is not None and name not in only:
+            continue
         w0 = torch.randn(shp, device=dev, generator=g) * 0.02
         w1 = w0 - 1e-5 * torch.randn(shp, device=dev, generator=g)
         base.append(DeviceTensor.wrap(name, w0.to(torch.bfloat16)))
@@ -77,13 +103,17 @@ def generate(config: str, dev, seed: int = 0):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--config", default="C0", choices=["C0", "C3"])
+    ap.add_argument("--config", default="C0", choices=["C0", "C3", "C4"])
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--verify", action="store_true")
+    ap.add_argument("--shard", default=None,
+                    help="R/W: only rank R's tensors of a W-rank plan (C4 needs 8 GPUs' HBM)")
     args = ap.parse_args()
     import torch
     from paper_2511_12376_b200 import store as S
     dev = torch.device("cuda:0")
+    if args.shard or args.config == "C4":
+        return run_shard(args, *(int(x) for x in (args.shard or "0/8").split("/")))
     c0, c1 = generate(args.config, dev)
     raw = sum(t.nbytes for t in c1.model_states + c1.optimizer_states)
     enc = S.CheckpointEncoder(dev, clusters=16)
@@ -149,6 +179,74 @@ def main():
         line["oracle_delta_encode_s"] = round(time.perf_counter() - t, 2)
         line["oracle_blob_identical"] = want == blob1
         line["oracle_manifest_identical"] = entries == [vars(e) for e in m1.tensors]
+    print(json.dumps(line), flush=True)
+
+
+def run_shard(args, rank: int, world: int):
+    """One rank's share of a multi-GPU save: the tensors the LPT plan gives
+    `rank`, encoded on this GPU (the ranks share nothing but the size-table
+    all-gather, so the job's time is the slowest rank's).  The restore runs
+    after the inputs but the compared weights are freed (inputs and restored
+    states of a C4 shard do not fit one GPU together)."""
+    import torch
+    from paper_2511_12376_b200 import store as S
+    dev = torch.device("cuda:0")
+    only, plan = shard_names(args.config, rank, world)
+    c0, c1 = generate(args.config, dev, only=only)
+    raw = sum(t.nbytes for t in c1.model_states + c1.optimizer_states)
+    enc = S.CheckpointEncoder(dev, clusters=16)
+    import numpy as np
+    from paper_2511_12376_b200 import _runtime as rt
+
+    def pinned(n):
+        # page-locked by registration: the caching host allocator would
+        # round tens of GB up to the next power of two
+        a = np.empty(n, dtype=np.uint8)
+        assert rt.lib().bsnp_host_register(a.ctypes.data, n) == 0, "host register failed"
+        t = torch.from_numpy(a)
+        assert t.is_pinned()
+        return t
+    buf0 = pinned(S.blob_bound(c0))
+    buf1 = pinned(S.blob_bound(c1))
+
+    def timed(fn):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        out = fn()
+        torch.cuda.synchronize()
+        return out, time.perf_counter() - t
+    res = {}
+    for _ in range(args.reps):
+        (m0, b0), tb = timed(lambda: enc.encode(c0, None, S.KIND_BASE, out=buf0))
+        (m1, b1), td = timed(lambda: enc.encode(c1, None, S.KIND_DELTA, out=buf1))
+        for k, v in (("save_base_s", tb), ("save_delta_s", td)):
+            res[k] = min(res.get(k, 1e9), v)
+    peak_save = torch.cuda.max_memory_allocated(dev)
+    want = [t.flat() for t in c1.model_states]
+    del c0, c1, enc
+    torch.cuda.empty_cache()
+    out, tl = timed(lambda: S.decode_chain([(m0, b0), (m1, b1)], to_host=False))
+    res["load_s"] = tl
+    ok = all(torch.equal(a.data.view(torch.int16), b) for a, b in zip(out.model_states, want))
+    mlen = sum(e.length for e in m1.tensors if e.group == "model")
+    olen = sum(e.length for e in m1.tensors if e.group == "optimizer")
+    line = {"config": args.config, "shard": f"{rank}/{world}", "tensors": len(m1.tensors),
+            "raw_bytes": raw, "plan_load_max_over_mean": round(max(plan.load) * world /
+                                                                sum(plan.load), 4),
+            "input_bytes_on_gpu": sum(12 * t.num_elements for t in out.model_states),
+            "ratio_total": round(raw / b1.numel(), 4),
+            "ratio_weights_optimizer": [round(sum(t.nbytes for t in out.model_states) / mlen, 4),
+                                        round(sum(t.nbytes for t in out.optimizer_states) /
+                                              olen, 4)],
+            "save_base_gbs": round(raw / res["save_base_s"] / 1e9, 2),
+            "save_delta_gbs": round(raw / res["save_delta_s"] / 1e9, 2),
+            "load_gbs": round(raw / res["load_s"] / 1e9, 2),
+            **{k: round(v, 4) for k, v in res.items()},
+            "peak_gpu_bytes_save": peak_save,
+            "peak_gpu_bytes": torch.cuda.max_memory_allocated(dev),
+            "restored_weights_identical": ok,
+            "note": "one rank's shard on one GPU; device-resident inputs, blobs in pinned host "
+                    "memory (D2H / H2D included); load once, after freeing the inputs"}
     print(json.dumps(line), flush=True)
 
 
