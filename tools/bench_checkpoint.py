@@ -2,7 +2,9 @@
 """Whole-checkpoint codec benchmark (BASELINE configs[0] "C0" and [3] "C3").
 
 A checkpoint pair (base at iteration 0, delta at iteration 1) of a
-GPT-2-small (C0) or Llama-2-7B (C3) shaped model is generated on the GPU
+GPT-2-small (C0), Llama-2-7B (C3, with fp32 master weights among the
+optimizer states) or one rank's share of a Llama-2-70B (C4) shaped model is
+generated on the GPU
 (SURVEY §8(d) recipe: fp32 master w0 ~ N(0, 0.02), w1 = w0 - 1e-5 u, saved
 weights bf16; Adam m ~ N(0, 1e-3), v = N(0, 1e-3)^2, quantized per tensor
 with m = 16 clusters as store.encode_checkpoint does).  Timed with CUDA
@@ -92,6 +94,8 @@ def generate(config: str, dev, seed: int = 0, only=None):
         w1 = w0 - 1e-5 * torch.randn(shp, device=dev, generator=g)
         base.append(DeviceTensor.wrap(name, w0.to(torch.bfloat16)))
         cur.append(DeviceTensor.wrap(name, w1.to(torch.bfloat16)))
+        if config == "C3":   # BASELINE configs[3]: bf16 weights plus fp32 master, m and v
+            opt.append(DeviceTensor.wrap("master." + name, w1))
         del w0, w1
         opt.append(DeviceTensor.wrap("adam.m." + name,
                                      torch.randn(shp, device=dev, generator=g) * 1e-3))
@@ -112,8 +116,11 @@ def main():
     import torch
     from paper_2511_12376_b200 import store as S
     dev = torch.device("cuda:0")
-    if args.shard or args.config == "C4":
-        return run_shard(args, *(int(x) for x in (args.shard or "0/8").split("/")))
+    if args.shard or args.config in ("C3", "C4"):
+        # C3 (107.8 GB of states) and its restore do not fit one GPU together:
+        # the shard path frees the inputs before the restore
+        default = "0/8" if args.config == "C4" else "0/1"
+        return run_shard(args, *(int(x) for x in (args.shard or default).split("/")))
     c0, c1 = generate(args.config, dev)
     raw = sum(t.nbytes for t in c1.model_states + c1.optimizer_states)
     enc = S.CheckpointEncoder(dev, clusters=16)
@@ -223,6 +230,8 @@ def run_shard(args, rank: int, world: int):
             res[k] = min(res.get(k, 1e9), v)
     peak_save = torch.cuda.max_memory_allocated(dev)
     want = [t.flat() for t in c1.model_states]
+    inputs = sum(t.nbytes for t in list(c0.model_states) + list(c1.model_states)
+                 + list(c1.optimizer_states))
     del c0, c1, enc
     torch.cuda.empty_cache()
     out, tl = timed(lambda: S.decode_chain([(m0, b0), (m1, b1)], to_host=False))
@@ -233,7 +242,7 @@ def run_shard(args, rank: int, world: int):
     line = {"config": args.config, "shard": f"{rank}/{world}", "tensors": len(m1.tensors),
             "raw_bytes": raw, "plan_load_max_over_mean": round(max(plan.load) * world /
                                                                 sum(plan.load), 4),
-            "input_bytes_on_gpu": sum(12 * t.num_elements for t in out.model_states),
+            "input_bytes_on_gpu": inputs,
             "ratio_total": round(raw / b1.numel(), 4),
             "ratio_weights_optimizer": [round(sum(t.nbytes for t in out.model_states) / mlen, 4),
                                         round(sum(t.nbytes for t in out.optimizer_states) /
