@@ -182,6 +182,15 @@ int bsnp_cluster_dequantize_batch(const bsnp_dequant_item* items, const uint32_t
                                   uint32_t nitems, uint32_t nchunks, bsnp_status* status,
                                   void* stream);
 
+/*
+ * n bytes from device memory to page-locked host memory (dst: a pinned or
+ * registered host address, device-accessible under unified addressing) by
+ * SM stores, not a copy engine: the encoder's status words and cluster
+ * tables come back without queueing behind the bulk device-to-host copies
+ * of earlier record groups (store.py:240-270 reads them synchronously).
+ */
+int bsnp_copy_sm(const void* src, void* dst, uint64_t n, void* stream);
+
 /* ------------------------------------------------------------------------
  * Checkpoint blob assembly
  * ---------------------------------------------------------------------- */

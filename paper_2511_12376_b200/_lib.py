@@ -37,6 +37,7 @@ SIGNATURES = {
     "bsnp_cluster_dequantize": (_i32, [_vp, _vp, _u64, _u64, _vp, _vp, _vp, _vp, _sz, _vp]),
     "bsnp_precision_report": (_i32, [_vp, _vp, _u64, _vp, _vp]),
     "bsnp_gather_segments": (_i32, [_vp, _vp, _c.c_uint32, _c.c_uint32, _vp, _vp]),
+    "bsnp_copy_sm": (_i32, [_vp, _vp, _u64, _vp]),
     "bsnp_cluster_dequantize_batch": (_i32, [_vp, _vp, _c.c_uint32, _c.c_uint32, _vp, _vp]),
 }
 

@@ -114,7 +114,35 @@ __global__ void __launch_bounds__(256)
     for (uint32_t i = head + nw * 4 + threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
   }
 }
+
+// small results to page-locked host memory through the SMs' stores rather
+// than a copy engine: the read-back does not queue behind bulk
+// device-to-host copies on other streams
+__global__ void __launch_bounds__(256)
+    copy_sm_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, uint64_t n) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (((((uintptr_t)src) | ((uintptr_t)dst)) & 15) == 0) {
+    const uint64_t nv = n / 16;
+    for (uint64_t i = t0; i < nv; i += stride)
+      reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+    for (uint64_t i = nv * 16 + t0; i < n; i += stride) dst[i] = src[i];
+  } else {
+    for (uint64_t i = t0; i < n; i += stride) dst[i] = src[i];
+  }
+}
 }  // namespace
+
+extern "C" int bsnp_copy_sm(const void* src, void* dst, uint64_t n, void* stream) {
+  if (n == 0) return BSNP_OK;
+  if (!src || !dst) return BSNP_E_INVALID;
+  uint64_t grid = (n / 16 + 255) / 256;
+  if (grid < 1) grid = 1;
+  if (grid > 148) grid = 148;
+  copy_sm_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(
+      static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), n);
+  return bsnp::launch_status("copy_sm_kernel");
+}
 
 extern "C" int bsnp_gather_segments(const bsnp_segment* segs, const uint32_t* first,
                                     uint32_t nsegs, uint32_t nchunks, uint8_t* blob,

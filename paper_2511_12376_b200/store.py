@@ -38,7 +38,7 @@ from . import _runtime as rt
 from . import bitmask as B
 from . import quantizer as Q
 from .tensors import (ByteCursor, Checkpoint, ElementType, TENSOR_MAGIC, FORMAT_VERSION,
-                      TensorBlob, UnsupportedVersionError, tensor_header)
+                      TensorBlob, UnsupportedVersionError, tensor_header, tensor_header_size)
 
 KIND_BASE = "base"
 KIND_DELTA = "delta"
@@ -351,11 +351,12 @@ class CheckpointEncoder:
                 "ndelta": sum(1 for p in steps if p[0] == "delta")}
 
     def _outputs(self, plan):
-        """The host-visible outputs of a launch sequence: the pinned copy of
-        every cluster table and the delta status words."""
+        """The host-visible outputs of a launch sequence: one pinned buffer
+        receiving the delta status words, then every cluster table."""
         n_tab = plan["sizes"][4]
-        tab_h = torch.empty(max(n_tab, 1) * Q.TABLE_BYTES, dtype=torch.uint8, pin_memory=True)
         st = rt.new_status(self.dev, max(plan["ndelta"], 1))
+        tab_h = torch.empty(st.numel() * 8 + max(n_tab, 1) * Q.TABLE_BYTES, dtype=torch.uint8,
+                            pin_memory=True)
         return tab_h, st
 
     def _run(self, plan, tab_h, st):
@@ -386,7 +387,12 @@ class CheckpointEncoder:
             launched += 1
         for ss in self._side:
             main.wait_stream(ss)
-        tab_h.copy_(tab_a, non_blocking=True)
+        # results come back by SM stores, not queued behind the copy engine's
+        # bulk transfers of earlier groups (pipelined save)
+        lib, sp, ns = rt.lib(), rt.stream_ptr(dev), st.numel() * 8
+        _lib.check(lib.bsnp_copy_sm(st.data_ptr(), tab_h.data_ptr(), ns, sp), "bsnp_copy_sm")
+        _lib.check(lib.bsnp_copy_sm(tab_a.data_ptr(), tab_h.data_ptr() + ns, tab_a.numel(), sp),
+                   "bsnp_copy_sm")
         return {"plan": plan, "arenas": (mask_a, pay_a, lab_a, code_a, tab_a),
                 "tab_h": tab_h, "st": st, "deltas": deltas, "quants": quants}
 
@@ -419,8 +425,12 @@ class CheckpointEncoder:
         then the codec decisions and the unplaced records."""
         plan = state["plan"]
         mask_a, pay_a, lab_a, code_a, _ = state["arenas"]
-        status = rt.read_status(state["st"])
-        tab_raw = state["tab_h"].numpy().tobytes()
+        torch.cuda.current_stream(self.dev).synchronize()
+        ns = state["st"].numel() * 8
+        hb = state["tab_h"].numpy()
+        status = [(int(r[0]), int(r[1]) & 0xFFFFFFFF)
+                  for r in hb[:ns].view(np.uint64).reshape(-1, 2).tolist()]
+        tab_raw = hb[ns:].tobytes()
         recs = {}
         for (p, di) in state["deltas"]:
             _, gid, t, flat, bflat, mo, po = p
@@ -597,11 +607,11 @@ def blob_bound(ckpt: Checkpoint) -> int:
     per element plus a header at most 256 bytes longer than the RAW one."""
     b = 0
     for t in ckpt.model_states:
-        b += len(tensor_header(t.name, t.dtype, t.shape)) + t.nbytes + 256
+        b += tensor_header_size(t.name, len(t.shape)) + t.nbytes + 256
     for t in ckpt.optimizer_states:
         n = t.num_elements
         body = (n + 1) // 2 + n if t.dtype is ElementType.F32 else t.nbytes
-        b += len(tensor_header(t.name, t.dtype, t.shape)) + body + 256
+        b += tensor_header_size(t.name, len(t.shape)) + body + 256
     return b
 
 
