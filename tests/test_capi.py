@@ -72,6 +72,8 @@ def test_batch_layouts_and_errors_without_gpu():
     assert lib.bsnp_cluster_dequantize_batch(None, None, 0, 0, None, None) == _lib.BSNP_OK
     assert lib.bsnp_cluster_dequantize_batch(None, None, 1, 1, None, None) \
         == _lib.BSNP_E_INVALID
+    assert lib.bsnp_copy_sm(None, None, 0, None) == _lib.BSNP_OK
+    assert lib.bsnp_copy_sm(None, None, 5, None) == _lib.BSNP_E_INVALID
 
 
 def test_quant_header_from_device_table_bytes():

@@ -322,3 +322,19 @@ def test_chain_replay_uploads_only_needed_spans(dev, checkpoint_golden, golden_i
     cut = S.decode_chain([(m0, g["blob0"].tobytes()[:end]), (m1, g["blob1"].tobytes())])
     assert [t.data for t in full.model_states] == [t.data for t in cut.model_states]
     assert [t.data for t in full.optimizer_states] == [t.data for t in cut.optimizer_states]
+
+
+def test_copy_sm_into_pinned_host(dev):
+    """bsnp_copy_sm: device bytes land in page-locked host memory by SM
+    stores (aligned vector path and byte path), nothing outside the range."""
+    from paper_2511_12376_b200 import _lib
+    from paper_2511_12376_b200 import _runtime as rt
+    src = torch.randint(0, 256, (1 << 20,), dtype=torch.uint8, device=dev)
+    want = src.cpu()
+    for so, do, n in ((0, 0, 1 << 20), (16, 32, 4096), (3, 0, 77), (5, 7, 99997), (0, 0, 1)):
+        dst = torch.zeros((1 << 20) + 64, dtype=torch.uint8, pin_memory=True)
+        _lib.check(rt.lib().bsnp_copy_sm(src.data_ptr() + so, dst.data_ptr() + do, n,
+                                         rt.stream_ptr(dev)), "bsnp_copy_sm")
+        torch.cuda.current_stream(dev).synchronize()
+        assert torch.equal(dst[do:do + n], want[so:so + n])
+        assert int(dst[:do].sum()) == 0 and int(dst[do + n:].sum()) == 0
