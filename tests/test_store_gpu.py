@@ -338,3 +338,46 @@ def test_copy_sm_into_pinned_host(dev):
         torch.cuda.current_stream(dev).synchronize()
         assert torch.equal(dst[do:do + n], want[so:so + n])
         assert int(dst[:do].sum()) == 0 and int(dst[do + n:].sum()) == 0
+
+
+def test_multi_chunk_restore_vs_oracle(dev):
+    """A chain whose links upload in 8 chunks, records straddling chunk
+    boundaries: the grouped restore (one gather and one batched dequantize
+    per chunk, deltas on side streams) rebuilds the weights bit for bit and
+    the optimizer states as the oracle's dequantize, from host bytes and
+    from pinned blobs alike."""
+    rng = np.random.default_rng(7)
+    sizes = [1, 7, 1000, 65535, 65537, 300001, 1 << 20, 777777, 3, 123457, 1 << 19, 2,
+             999999, 4096, 250000]
+    frac = [1.0, 0.0, 0.3, 0.01, 0.0, 0.05, 0.02, 1.0, 0.5, 0.001, 0.2, 1.0, 0.04, 0.6, 0.0]
+    model0, model1, opt = [], [], []
+    for i, (n, f) in enumerate(zip(sizes, frac)):
+        a = rng.integers(0, 1 << 16, n, dtype=np.uint16)
+        b = a.copy()
+        k = int(n * f)
+        if k:
+            idx = rng.choice(n, k, replace=False)
+            b[idx] ^= rng.integers(1, 1 << 16, k, dtype=np.uint16)
+        model0.append(TensorBlob(f"w{i}", ElementType.F16, (n,), a.tobytes()))
+        model1.append(TensorBlob(f"w{i}", ElementType.F16, (n,), b.tobytes()))
+        if n > 1:
+            opt.append(TensorBlob(f"m{i}", ElementType.F32, (n,),
+                                  (rng.standard_normal(n) * 1e-3).astype(np.float32).tobytes()))
+    c0 = Checkpoint(iteration=1, model_states=model0, optimizer_states=opt)
+    c1 = Checkpoint(iteration=2, model_states=model1, optimizer_states=opt)
+    enc = S.CheckpointEncoder(dev, clusters=16)
+    m0, b0 = enc.encode(c0, None, S.KIND_BASE)
+    m1, b1 = enc.encode(c1, None, S.KIND_DELTA)
+    codecs = {e.codec for e in m1.tensors if e.group == S.GROUP_MODEL}
+    assert codecs == {"RAW", "DELTA"}
+    want_opt = []
+    for t in opt:
+        x = np.frombuffer(t.data, np.float32)
+        tab = O.cluster_fit(x, 16)
+        p, c, _ = O.cluster_quantize(x, tab)
+        want_opt.append(O.cluster_dequantize(p, c, x.size, tab).astype("<f4").tobytes())
+    for chain in ([(m0, b0.numpy().tobytes()), (m1, b1.numpy().tobytes())],
+                  [(m0, b0), (m1, b1)]):
+        rec = S.decode_chain(chain)
+        assert [t.data for t in rec.model_states] == [t.data for t in model1]
+        assert [t.data for t in rec.optimizer_states] == want_opt
