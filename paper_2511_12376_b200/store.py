@@ -488,11 +488,12 @@ class CheckpointEncoder:
         returned) — page-locking a fresh multi-GB buffer per save costs
         seconds, so a training loop passes its own (e.g. two alternating
         buffers); a new one is allocated when it is missing or too small."""
-        if out is not None and out.is_pinned() and self._groups(ckpt) > 1:
+        if out is not None and out.is_pinned():
             buf = out.reshape(-1).view(torch.uint8)
             raw = sum(t.nbytes for t in list(ckpt.model_states) + list(ckpt.optimizer_states))
-            if raw > self.pipeline_min_bytes and buf.numel() >= blob_bound(ckpt):
-                return self._encode_pipelined(ckpt, prev, kind, buf)
+            ng = self._groups(raw)
+            if ng > 1 and raw > self.pipeline_min_bytes and buf.numel() >= blob_bound(ckpt):
+                return self._encode_pipelined(ckpt, prev, kind, buf, ng)
 
         def dest(manifest, nbytes):
             if out is not None and out.is_pinned() and out.numel() >= nbytes:
@@ -500,13 +501,12 @@ class CheckpointEncoder:
             return torch.empty(max(nbytes, 1), dtype=torch.uint8, pin_memory=True)[:nbytes]
         return self.encode_into(ckpt, prev, kind, dest)
 
-    def _groups(self, ckpt) -> int:
+    def _groups(self, raw: int) -> int:
         if self.pipeline_groups is not None:
             return self.pipeline_groups
-        raw = sum(t.nbytes for t in list(ckpt.model_states) + list(ckpt.optimizer_states))
         return 3 if raw <= GRAPH_MAX_ARENA else 8
 
-    def _encode_pipelined(self, ckpt, prev, kind, buf):
+    def _encode_pipelined(self, ckpt, prev, kind, buf, ng: int):
         """encode() into a caller buffer that can hold any outcome: the
         tensors go in a few groups, and while group g+1 is encoded the
         records of group g (their offsets known from group g's one sync)
@@ -516,7 +516,6 @@ class CheckpointEncoder:
         k = len(items)
         items += [(k + i, GROUP_OPTIMIZER, t) for i, t in enumerate(ckpt.optimizer_states)]
         total = sum(t.nbytes for _, _, t in items)
-        ng = self._groups(ckpt)
         groups, cur, acc = [], [], 0
         for it in items:
             cur.append(it)
