@@ -25,6 +25,7 @@ The file-system lifecycle (tracker, commit, recovery, pruning) is out of scope
 from __future__ import annotations
 
 import bisect
+import functools
 import json
 import os
 import struct
@@ -212,7 +213,7 @@ class EncodedRecord:
     header: bytes
     parts: list
 
-    @property
+    @functools.cached_property
     def length(self) -> int:
         return len(self.header) + sum(_part_nbytes(p) for p in self.parts)
 
