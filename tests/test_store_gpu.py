@@ -302,7 +302,7 @@ def test_pipelined_save_into_caller_buffer(dev, checkpoint_golden, golden_index,
     c0, c1 = _golden_ckpts(g, meta)
     enc = S.CheckpointEncoder(dev, clusters=16, keep_prev=False)
     enc.pipeline_groups = groups
-    enc.pipeline_min_bytes = 0      # the golden checkpoint is small: force the path
+    enc.pipeline_min_bytes = 0      # (the default) any size takes the pipelined path
     buf = torch.empty(S.blob_bound(c1) + 7, dtype=torch.uint8, pin_memory=True)
     for ck, prev, kind, bkey, mkey in ((c0, None, S.KIND_BASE, "blob0", "manifest0"),
                                        (c1, c0, S.KIND_DELTA, "blob1", "manifest1")):
