@@ -870,6 +870,7 @@ def decode_chain(chain, device: torch.device | None = None, to_host: bool = True
             dblob = torch.empty(need, dtype=torch.uint8, device=dev)
             links.append((manifest, mv, dblob, _ChunkedUpload(pin, dblob, need, dev)))
         checks = []        # deferred device checks, in the reference's raise order
+        keep = []          # pinned metadata the queued kernels read
         try:
             for ci, (manifest, mv, dblob, ready) in enumerate(links):
                 final = ci == len(links) - 1
@@ -877,7 +878,7 @@ def decode_chain(chain, device: torch.device | None = None, to_host: bool = True
                 if manifest.kind == KIND_BASE:
                     model_order = [e.name for e in manifest.tensors if e.group == GROUP_MODEL]
                 plan.check_deltas(model, meta)
-                opt = plan.launch(dev, dblob, model, meta, checks)
+                opt = plan.launch(dev, dblob, model, meta, checks, keep)
                 if final:
                     final_opt = opt
                 ready.finish()
@@ -885,6 +886,7 @@ def decode_chain(chain, device: torch.device | None = None, to_host: bool = True
                 # are ordered before anything the current stream queues next)
                 links[ci] = dblob = None
         except Exception:
+            torch.cuda.current_stream(dev).synchronize()
             _run_checks(checks)  # an earlier link's device error is reported first
             raise
         _run_checks(checks)
@@ -1051,7 +1053,7 @@ class _LinkPlan:
             if base.dtype != torch.int16:
                 raise B.DeltaError("delta encoding requires F16 tensors")
 
-    def launch(self, dev, dblob, model, meta, checks) -> list:
+    def launch(self, dev, dblob, model, meta, checks, keep) -> list:
         """Queues the link; returns the final link's optimizer states."""
         lib = rt.lib()
         nchunk = max(len(self.ready.bounds), 1)
@@ -1131,7 +1133,11 @@ class _LinkPlan:
                 items = (mbase + io, mbase + fi, len(items), int(fst[-1]),
                          sbase + 16 * (nd + items[0]))
             launches.append((segs, items))
-        mdev.copy_(host, non_blocking=True)
+        # by SM loads from the pinned buffer: a copy-engine upload would
+        # queue behind the bulk chunks of every link queued before it
+        _lib.check(lib.bsnp_copy_sm(host.data_ptr(), mdev.data_ptr(), host.numel(),
+                                    rt.stream_ptr(dev)), "bsnp_copy_sm")
+        keep.append(host)   # read asynchronously: alive until the restore synchronises
         lanes = _Lanes(dev)
         # the delta decodes go round-robin over the lanes; a chunk's gather
         # runs first on its own lane (realigned payloads), so deltas needing
