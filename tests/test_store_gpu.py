@@ -381,3 +381,16 @@ def test_multi_chunk_restore_vs_oracle(dev):
         rec = S.decode_chain(chain)
         assert [t.data for t in rec.model_states] == [t.data for t in model1]
         assert [t.data for t in rec.optimizer_states] == want_opt
+    # a third link: the middle link now contributes only its model span
+    model2 = []
+    for t in model1:
+        a = np.frombuffer(t.data, np.uint16).copy()
+        k = a.size // 3
+        if k:
+            a[rng.choice(a.size, k, replace=False)] += 1
+        model2.append(TensorBlob(t.name, ElementType.F16, t.shape, a.tobytes()))
+    c2 = Checkpoint(iteration=3, model_states=model2, optimizer_states=opt)
+    m2, b2 = enc.encode(c2, None, S.KIND_DELTA)
+    rec = S.decode_chain([(m0, b0), (m1, b1.numpy().tobytes()), (m2, b2)])
+    assert [t.data for t in rec.model_states] == [t.data for t in model2]
+    assert [t.data for t in rec.optimizer_states] == want_opt
