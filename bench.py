@@ -337,6 +337,9 @@ def run_b200(args, rank: int, world: int, local_rank: int):
         line["c0_checkpoint"] = c0
     if world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(args.p, args.cpu_elems_per_core)
+        # the 1-core figure beside the all-core one
+        one = cpu_baseline(args.p, args.cpu_elems_per_core, cores=1)
+        line["cpu_baseline"]["value_1core"] = one["value"]
     print(json.dumps(line), flush=True)
 
 
