@@ -285,18 +285,25 @@ def _dist(name, n, rng):
     raise ValueError(name)
 
 
-@pytest.mark.parametrize("log2b,units,tail", [(13, 5, 0), (16, 3, 1000), (20, 2, 8),
-                                               (21, 1, 0)])
-@pytest.mark.parametrize("dist", ["adam_m", "adam_v", "discrete", "sparse", "offset",
-                                  "uniform"])
-@pytest.mark.parametrize("m", [16, 7, 2])
+_DISTS = ["adam_m", "adam_v", "discrete", "sparse", "offset", "uniform"]
+
+
+def _cases(shapes, keep):
+    """shape x distribution x m, minus the large combinations the CPU
+    oracle's time budget leaves out (`keep` says which large ones stay)."""
+    return [(lb, u, t, d, m) for lb, u, t in shapes for d in _DISTS for m in (16, 7, 2)
+            if keep(lb, d, m)]
+
+
+@pytest.mark.parametrize("log2b,units,tail,dist,m", _cases(
+    [(13, 5, 0), (16, 3, 1000), (20, 2, 8), (21, 1, 0)],
+    lambda lb, d, m: not ((lb >= 20 and m != 16) or (lb == 21 and d not in ("adam_m",
+                                                                            "discrete")))))
 def test_power_of_two_blocks_vs_oracle(dev, log2b, units, tail, dist, m):
     """Power-of-two blocks of 2^13..2^21 (perfect tree tiles) plus a ragged
     tail unit; sparse/discrete data force the exact min/max round.  Every
     unit is bit-exact vs the oracle, and the fit-only path gives the same
     tables."""
-    if (log2b >= 20 and m != 16) or (log2b == 21 and dist not in ("adam_m", "discrete")):
-        pytest.skip("size budget")
     from paper_2511_12376_b200 import quantizer as Q
     block = 1 << log2b
     n = units * block + tail
@@ -326,19 +333,15 @@ def test_repeatable_and_nonfinite(dev):
         Q.cluster_encode_device(x, 16, block)
 
 
-@pytest.mark.parametrize("log2b,units,tail", [(13, 9, 0), (13, 8, 100), (16, 8, 1000),
-                                               (17, 10, 8), (20, 8, 0)])
-@pytest.mark.parametrize("dist", ["adam_m", "adam_v", "discrete", "sparse", "offset",
-                                  "uniform"])
-@pytest.mark.parametrize("m", [16, 7, 2])
+@pytest.mark.parametrize("log2b,units,tail,dist,m", _cases(
+    [(13, 9, 0), (13, 8, 100), (16, 8, 1000), (17, 10, 8), (20, 8, 0)],
+    lambda lb, d, m: not (lb == 20 and (m != 16 or d not in ("adam_m", "discrete")))))
 def test_many_units_vs_oracle(dev, log2b, units, tail, dist, m):
     """Encodes of 8-10 units plus a ragged tail: one-sided data (adam_v: the
     lower fit thresholds lie below every element, so those clusters are
     empty and decided from the unit extremes), constant blocks (decided
     directly), discrete / sparse data (the exact min/max round).  Bit-exact
     vs the oracle."""
-    if log2b == 20 and (m != 16 or dist not in ("adam_m", "discrete")):
-        pytest.skip("size budget")
     from paper_2511_12376_b200 import quantizer as Q
     block = 1 << log2b
     n = units * block + tail
