@@ -394,3 +394,31 @@ def test_multi_chunk_restore_vs_oracle(dev):
     rec = S.decode_chain([(m0, b0), (m1, b1.numpy().tobytes()), (m2, b2)])
     assert [t.data for t in rec.model_states] == [t.data for t in model2]
     assert [t.data for t in rec.optimizer_states] == want_opt
+
+
+def test_save_and_restore_through_registered_host_memory(dev, checkpoint_golden, golden_index):
+    """Landing buffers page-locked by registration (bsnp_host_register on a
+    plain host allocation, as for tens-of-GB checkpoints) behave as pinned
+    ones: same blobs as the reference, same restore."""
+    from paper_2511_12376_b200 import _runtime as rt
+    g, meta = checkpoint_golden, golden_index["checkpoint"]
+    c0, c1 = _golden_ckpts(g, meta)
+    enc = S.CheckpointEncoder(dev, clusters=16)
+    arrs, bufs = [], []
+    for ck in (c0, c1):
+        a = np.zeros(S.blob_bound(ck) + 64, dtype=np.uint8)
+        assert rt.lib().bsnp_host_register(a.ctypes.data, a.nbytes) == 0
+        arrs.append(a)
+        bufs.append(torch.from_numpy(a))
+    try:
+        assert all(b.is_pinned() for b in bufs)
+        m0, b0 = enc.encode(c0, None, S.KIND_BASE, out=bufs[0])
+        m1, b1 = enc.encode(c1, None, S.KIND_DELTA, out=bufs[1])
+        assert b0.numpy().tobytes() == g["blob0"].tobytes()
+        assert b1.numpy().tobytes() == g["blob1"].tobytes()
+        rec = S.decode_chain([(m0, b0), (m1, b1)])
+        assert [t.data for t in rec.model_states] == [t.data for t in c1.model_states]
+    finally:
+        torch.cuda.synchronize()
+        for a in arrs:
+            rt.lib().bsnp_host_unregister(a.ctypes.data)
