@@ -48,7 +48,29 @@ def workspace(device: torch.device, nbytes: int, slot: str = "ws") -> torch.Tens
         buf = torch.empty((max(int(nbytes * 1.25), 256) + 255) // 256 * 256, dtype=torch.uint8,
                           device=device)
         c[key] = buf
+    keep = getattr(_tls, "keep", None)
+    if keep is not None:
+        keep.append(buf)
     return buf
+
+
+class keep_workspaces:
+    """Collect every workspace handed out inside the block (e.g. while a CUDA
+    graph is captured): the graph records their addresses, so its owner must
+    keep them alive for as long as it may replay — the per-thread cache may
+    swap in a bigger buffer and free the captured one."""
+
+    def __enter__(self):
+        self.prev = getattr(_tls, "keep", None)
+        self.bufs = []
+        _tls.keep = self.bufs
+        return self.bufs
+
+    def __exit__(self, *exc):
+        _tls.keep = self.prev
+        if self.prev is not None:
+            self.prev.extend(self.bufs)
+        return False
 
 
 def new_status(device: torch.device, count: int = 1) -> torch.Tensor:

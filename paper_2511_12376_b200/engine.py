@@ -296,10 +296,90 @@ class SlotRegion:
             self._mm[off:off + len(head)] = head
             return view[off + len(head):off + total]
 
-        manifest, _ = encoder.encode_into(ckpt, prev, kind, dest)
+        try:
+            manifest, _ = encoder.encode_into(ckpt, prev, kind, dest)
+        except BaseException:
+            # a failed copy (e.g. out of device memory) must not leave the
+            # slot WRITING for good: _claim never reuses such a slot
+            if "idx" in claimed:
+                with self._lock:
+                    self.clear_slot(rank, claimed["idx"])
+            raise
         with self._lock:
             info = self._seal(rank, claimed["idx"], ckpt.iteration, claimed["total"])
         return info, manifest
+
+
+def rank_store(parent_root, rank: int, **cfg_kwargs):
+    """engine.py:230-232: each rank persists into its own store root."""
+    from .fsstore import StoreConfig
+    return StoreConfig(root=Path(parent_root) / f"rank_{rank:02d}", **cfg_kwargs)
+
+
+class AsyncAgent:
+    """engine.py:235-306: the background consumer that persists VALID slots
+    through the store (unpack_blob + commit, oldest iteration first per rank;
+    a failed commit keeps the slot VALID for a retry and is recorded in
+    `errors`).  Pure host work: the codec ran when the slot was staged."""
+
+    def __init__(self, region: SlotRegion, store_root, poll_interval: float = 0.01,
+                 **store_kwargs):
+        self.region = region
+        self.store_root = Path(store_root)
+        self.poll_interval = poll_interval
+        self.store_kwargs = store_kwargs
+        self.errors: list = []
+        self._stop = threading.Event()
+        self._thread = None
+
+    def rank_config(self, rank: int):
+        return rank_store(self.store_root, rank, **self.store_kwargs)
+
+    def persist_once(self) -> int:
+        from . import store as S
+        done = 0
+        for rank in range(self.region.ranks):
+            pending = sorted((s for s in self.region.slots(rank) if s.state == STATE_VALID),
+                             key=lambda s: s.iteration)
+            for info in pending:
+                if not self.region.verify(rank, info.index):
+                    self.errors.append(f"rank {rank} iteration {info.iteration}: "
+                                       "checksum mismatch")
+                    continue
+                try:
+                    manifest, tensors = S.unpack_blob(self.region.payload(rank, info.index))
+                    S.commit(self.rank_config(rank), manifest, tensors)
+                except Exception as exc:  # keep the slot VALID for a retry
+                    self.errors.append(f"rank {rank} iteration {info.iteration}: {exc}")
+                    continue
+                self.region.set_state(rank, info.index, STATE_PERSISTED)
+                done += 1
+        return done
+
+    def persist_loop(self) -> None:
+        while not self._stop.is_set():
+            if self.persist_once() == 0:
+                self._stop.wait(self.poll_interval)
+
+    def start(self) -> None:
+        self._stop.clear()
+        self._thread = threading.Thread(target=self.persist_loop, daemon=True)
+        self._thread.start()
+
+    def stop(self) -> None:
+        self._stop.set()
+        if self._thread is not None:
+            self._thread.join()
+            self._thread = None
+
+    def drain(self, timeout: float = 30.0) -> None:
+        import time
+        deadline = time.monotonic() + timeout
+        while time.monotonic() < deadline:
+            if not any(s.state == STATE_VALID for s in self.region.all_slots()):
+                return
+            time.sleep(0.002)
+        raise EngineError("timed out waiting for agent to drain slots")
 
 
 def status_report(region: SlotRegion) -> str:

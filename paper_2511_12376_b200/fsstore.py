@@ -1,0 +1,227 @@
+"""The reference store's save / load entry points over the B200 codec.
+
+`save_checkpoint(cfg, ckpt, prev)` and `load_checkpoint(cfg, iteration)`
+(/root/reference/pkg/src/bitsnap/store.py:374-392, 418-474) are the callers
+of the hot path: save = the base-refresh policy (decide_kind, store.py:306-
+323) + encode_checkpoint (GPU) + commit (store.py:339-371); load = walk the
+manifests back to the anchoring base, then ONE `decode_chain` on the GPU
+(in-place delta apply, batched dequantize).  The on-disk layout — iter_NNNNNNN
+directories holding tensors.bin / manifest.bin / type.txt, the tracker file,
+the needs-base marker, the lock file — is the reference's, so either
+implementation reads what the other wrote.
+
+Kept deliberately thin: the reference's crash-point hooks (faults.py), inspect
+and pruning are store maintenance, not codec work; this module is
+the byte sink and source around the device codec.
+"""
+
+from __future__ import annotations
+
+import os
+import shutil
+from dataclasses import dataclass
+from pathlib import Path
+
+from filelock import FileLock
+
+TRACKER_NAME = "latest_checkpointed_iteration.txt"
+LOCK_NAME = ".lock"
+NEEDS_BASE_MARKER = ".needs_base"
+DIR_PREFIX = "iter_"
+DIR_DIGITS = 7
+
+
+def _errors():
+    from . import store as S
+    return S
+
+
+class TrackerError(RuntimeError):
+    pass
+
+
+class MissingLinkError(RuntimeError):
+    def __init__(self, iteration: int):
+        super().__init__(f"checkpoint directory for iteration {iteration} is missing")
+        self.iteration = iteration
+
+
+@dataclass
+class StoreConfig:
+    """store.py:84-111 (same fields, same MAX_CACHED_ITERATION override)."""
+
+    root: Path
+    max_cached_iteration: int = 1
+    redundancy_depth: int = 2
+    quantizer_clusters: int = 16
+
+    def __post_init__(self):
+        self.root = Path(self.root)
+        S = _errors()
+        if self.effective_max_cached() < 1:
+            raise S.StoreError("max_cached_iteration must be >= 1")
+        if self.redundancy_depth < 1:
+            raise S.StoreError("redundancy depth must be >= 1")
+
+    def effective_max_cached(self) -> int:
+        env = os.environ.get("MAX_CACHED_ITERATION")
+        return int(env) if env is not None else self.max_cached_iteration
+
+    def tracker_path(self) -> Path:
+        return self.root / TRACKER_NAME
+
+    def iter_dir(self, iteration: int) -> Path:
+        return self.root / f"{DIR_PREFIX}{iteration:0{DIR_DIGITS}d}"
+
+    def lock(self) -> FileLock:
+        return FileLock(str(self.root / LOCK_NAME))
+
+
+def write_tracker(cfg: StoreConfig, latest: int, latest_base: int) -> None:
+    """store.py:181-187: temp file + atomic rename."""
+    path = cfg.tracker_path()
+    tmp = path.with_suffix(".tmp")
+    tmp.write_text(f"{latest}\n{latest_base}\n")
+    os.replace(tmp, path)
+
+
+def read_tracker(cfg: StoreConfig) -> tuple:
+    """store.py:190-201 -> (latest_iteration, latest_base_iteration)."""
+    path = cfg.tracker_path()
+    if not path.exists():
+        raise TrackerError(f"tracker file not found at {path}")
+    lines = path.read_text().splitlines()
+    if len(lines) < 2:
+        raise TrackerError(f"malformed tracker file at {path}")
+    try:
+        return int(lines[0]), int(lines[1])
+    except ValueError as exc:
+        raise TrackerError(f"malformed tracker file at {path}: {exc}") from exc
+
+
+def try_read_tracker(cfg: StoreConfig):
+    try:
+        return read_tracker(cfg)
+    except TrackerError:
+        return None
+
+
+def list_iterations(cfg: StoreConfig) -> list:
+    if not cfg.root.exists():
+        return []
+    out = []
+    for p in sorted(cfg.root.iterdir()):
+        if p.is_dir() and p.name.startswith(DIR_PREFIX):
+            try:
+                out.append(int(p.name[len(DIR_PREFIX):]))
+            except ValueError:
+                continue
+    return out
+
+
+def decide_kind(cfg: StoreConfig, iteration: int) -> str:
+    """store.py:306-323: a base, then max_cached_iteration - 1 deltas; a
+    failed delta save forces the next save to be a base."""
+    S = _errors()
+    if (cfg.root / NEEDS_BASE_MARKER).exists():
+        return S.KIND_BASE
+    tracker = try_read_tracker(cfg)
+    if tracker is None:
+        return S.KIND_BASE
+    since_base = sum(1 for it in list_iterations(cfg) if it >= tracker[1])
+    return S.KIND_BASE if since_base >= cfg.effective_max_cached() else S.KIND_DELTA
+
+
+def commit(cfg: StoreConfig, manifest, tensors) -> None:
+    """store.py:339-371: write one checkpoint directory, then advance the
+    tracker, under the store lock.  `tensors` may be bytes or a host uint8
+    tensor (the encoder's pinned output, written without a copy)."""
+    from .store import write_tensors_bin
+    S = _errors()
+    cfg.root.mkdir(parents=True, exist_ok=True)
+    final_dir = cfg.iter_dir(manifest.iteration)
+    tmp_dir = cfg.root / f".tmp_{final_dir.name}"
+    with cfg.lock():
+        try:
+            if tmp_dir.exists():
+                shutil.rmtree(tmp_dir)
+            tmp_dir.mkdir()
+            write_tensors_bin(str(tmp_dir / "tensors.bin"), tensors)
+            (tmp_dir / "manifest.bin").write_bytes(manifest.to_bytes())
+            (tmp_dir / "type.txt").write_text(manifest.kind + "\n")
+            os.replace(tmp_dir, final_dir)
+            prev = try_read_tracker(cfg)
+            if manifest.kind == S.KIND_BASE:
+                base = manifest.iteration
+            else:
+                base = prev[1] if prev else manifest.base_iteration
+            write_tracker(cfg, manifest.iteration, base)
+            marker = cfg.root / NEEDS_BASE_MARKER
+            if manifest.kind == S.KIND_BASE and marker.exists():
+                marker.unlink()
+        except Exception:
+            shutil.rmtree(tmp_dir, ignore_errors=True)
+            raise
+
+
+def save_checkpoint(cfg: StoreConfig, ckpt, prev=None, encoder=None):
+    """store.py:374-392 -> CheckpointManifest.
+
+    `encoder`: an optional `store.CheckpointEncoder` that keeps the previous
+    model states resident in HBM, so a delta save needs no `prev` (the
+    reference's service reloads the previous checkpoint from disk first,
+    app.py:62-64)."""
+    S = _errors()
+    kind = decide_kind(cfg, ckpt.iteration)
+    try:
+        if encoder is None:
+            encoder = S.CheckpointEncoder(clusters=cfg.quantizer_clusters, keep_prev=False)
+        elif encoder.clusters != cfg.quantizer_clusters:
+            raise S.StoreError(f"encoder uses {encoder.clusters} clusters, the store "
+                               f"{cfg.quantizer_clusters}")
+        manifest, out = encoder.encode(ckpt, prev, kind)
+        commit(cfg, manifest, out)
+    except Exception:
+        if kind == S.KIND_DELTA:
+            cfg.root.mkdir(parents=True, exist_ok=True)
+            (cfg.root / NEEDS_BASE_MARKER).touch()
+        raise
+    return manifest
+
+
+def read_manifest(cfg: StoreConfig, iteration: int):
+    """store.py:395-410."""
+    S = _errors()
+    d = cfg.iter_dir(iteration)
+    if not d.exists():
+        raise MissingLinkError(iteration)
+    manifest = S.CheckpointManifest.from_bytes((d / "manifest.bin").read_bytes())
+    token = (d / "type.txt").read_text().strip()
+    if token != manifest.kind:
+        raise S.StoreError(f"iteration {iteration}: type.txt says {token!r} but manifest "
+                           f"says {manifest.kind!r}")
+    if manifest.iteration != iteration:
+        raise S.StoreError(f"directory {d.name} holds manifest for iteration "
+                           f"{manifest.iteration}")
+    return manifest
+
+
+def load_checkpoint(cfg: StoreConfig, iteration: int | None = None, device=None,
+                    to_host: bool = True):
+    """store.py:418-474: reconstruct a saved checkpoint.  The chain of
+    manifests back to the anchoring base is read from disk, then replayed by
+    `decode_chain` on the GPU (model states bit-identical, optimizer states
+    dequantized exactly as the reference's dequantize)."""
+    S = _errors()
+    if iteration is None:
+        iteration = read_tracker(cfg)[0]
+    chain, it = [], iteration
+    while True:
+        manifest = read_manifest(cfg, it)
+        chain.append(manifest)
+        if manifest.kind == S.KIND_BASE:
+            break
+        it = manifest.base_iteration
+    chain.reverse()
+    links = [(m, (cfg.iter_dir(m.iteration) / "tensors.bin").read_bytes()) for m in chain]
+    return S.decode_chain(links, device=device, to_host=to_host)

@@ -198,10 +198,22 @@ def write_shard(path: str, res: ShardResult, device=None) -> int:
             os.ftruncate(fd, res.total_bytes)
         mv = memoryview(buf.numpy())
         for r, lo, go in zip(res.records, local_offs, res.offsets):
-            os.pwrite(fd, mv[lo:lo + r.length], go)
+            _pwrite_all(fd, mv[lo:lo + r.length], go)
     finally:
         os.close(fd)
     return local_offs[-1]
+
+
+def _pwrite_all(fd: int, mv: memoryview, offset: int) -> None:
+    """pwrite until every byte landed: Linux moves at most 0x7ffff000 bytes
+    per call, so a record of 2 GiB or more needs several."""
+    import os
+    done = 0
+    while done < len(mv):
+        k = os.pwrite(fd, mv[done:], offset + done)
+        if k <= 0:
+            raise OSError(f"pwrite wrote {k} bytes at offset {offset + done}")
+        done += k
 
 
 def _place(recs, offsets, buf, device):

@@ -233,19 +233,32 @@ def _raw_record(gid, t, group, dev_flat) -> EncodedRecord:
 class CheckpointEncoder:
     """encode_checkpoint (store.py:214-272) on one GPU.
 
-    `keep_prev=True` keeps the model states of the last encoded checkpoint
+    `keep_prev` keeps the model states of the last encoded checkpoint
     resident in HBM, so the next delta save needs no `prev` argument and no
-    host round trip of the previous checkpoint.
+    host round trip of the previous checkpoint:
+
+    * True / "copy" (default): device-resident inputs (the training
+      process's live parameter buffers, which the optimizer changes in place)
+      are copied into encoder-owned buffers after each save — one
+      device-to-device copy of the model states at HBM speed;
+    * "borrow": the inputs are referenced, not copied; the caller promises
+      not to mutate them before the next save (e.g. alternating snapshot
+      buffers).  A delta save whose inputs ARE the borrowed previous states
+      raises instead of silently encoding n_c = 0 everywhere;
+    * False: nothing is kept (every delta save passes `prev`).
     """
 
     def __init__(self, device: torch.device | None = None, clusters: int = 16, block: int = 0,
-                 keep_prev: bool = True):
+                 keep_prev: bool | str = True):
         Q._check_m(clusters)
+        if keep_prev not in (True, False, "copy", "borrow"):
+            raise ValueError(f"keep_prev must be True, False, 'copy' or 'borrow', not {keep_prev!r}")
         self.dev = rt.device_of() if device is None else torch.device(device)
         self.clusters = clusters
         self.block = block
         self.keep_prev = keep_prev
         self.prev = None            # (iteration, {name: device int16 flat tensor})
+        self._owned = {}            # name -> encoder-owned copy of a borrowed input
         # CUDA graphs of the launch sequence for device-resident inputs
         # (BSNP_GRAPHS=0 disables); a key is captured the second time it is seen
         self.graphs = os.environ.get("BSNP_GRAPHS", "1") != "0"
@@ -292,21 +305,24 @@ class CheckpointEncoder:
                 tab_h, st = self._outputs(plan)
                 torch.cuda.synchronize(dev)
                 g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g):
+                with rt.keep_workspaces() as kept, torch.cuda.graph(g):
                     state = self._run(plan, tab_h, st)
-                ent = self._graphs[key] = (g, state)
+                # the scratch buffers the graph writes stay owned by its entry
+                ent = self._graphs[key] = (g, state, kept)
             if ent is None:
                 self._seen.add(key)
                 return self._finish(self._run(plan, *self._outputs(plan)))
-            g, state = ent
+            g, state, _ = ent
             g.replay()
         return self._finish(state)
 
     def _graph_key(self, plan, kind):
         k = [kind, self.clusters, self.block]
         for p in plan["steps"]:
-            k.append((p[0], p[1], p[3].data_ptr(), p[3].numel(),
-                      p[4].data_ptr() if p[0] == "delta" else 0))
+            # _finish builds the records' headers from the captured plan, so
+            # names, layout tags and shapes are part of the key
+            k.append((p[0], p[1], p[2].name, p[2].dtype, p[2].shape, p[3].data_ptr(),
+                      p[3].numel(), p[4].data_ptr() if p[0] == "delta" else 0))
         return tuple(k)
 
     def _plan(self, items, prev_map, kind, up):
@@ -553,8 +569,7 @@ class CheckpointEncoder:
             iteration=ckpt.iteration, kind=kind, base_iteration=base_iter,
             tensors=tuple(ManifestEntry(r.name, r.group, r.codec, o, r.length)
                           for r, o in zip(all_recs, offsets)))
-        if self.keep_prev:
-            self.prev = (ckpt.iteration, model_dev)
+        self._retain(ckpt, model_dev)
         return manifest, buf[:offsets[-1]]
 
     def encode_into(self, ckpt: Checkpoint, prev: Checkpoint | None, kind: str, dest):
@@ -575,12 +590,37 @@ class CheckpointEncoder:
                           for r, o in zip(recs, offsets)))
         out = dest(manifest, offsets[-1])
         place_records(recs, offsets, out, self.dev)
-        if self.keep_prev:
-            # the device copies of host inputs become the next delta base;
-            # device-resident inputs are referenced (the caller owns them and
-            # must not mutate them before the next save, or pass prev)
-            self.prev = (ckpt.iteration, model_dev)
+        self._retain(ckpt, model_dev)
         return manifest, out
+
+    def _retain(self, ckpt, model_dev) -> None:
+        """Keep this save's model states as the next delta base.  The device
+        copies of host inputs are the encoder's own already; device-resident
+        inputs are the caller's live buffers and are copied (mode "copy") into
+        encoder-owned buffers on the current stream, after every launch that
+        read them."""
+        if not self.keep_prev:
+            return
+        if self.keep_prev == "borrow":
+            self.prev = (ckpt.iteration, model_dev)
+            return
+        kept = {}
+        with torch.cuda.device(self.dev):
+            for t in ckpt.model_states:
+                flat = model_dev[t.name]
+                if not (isinstance(t, DeviceTensor) and _shares_storage(flat, t.data)):
+                    kept[t.name] = flat      # an upload or a contiguous copy: ours
+                    continue
+                own = self._owned.get(t.name)
+                if own is None or own.numel() != flat.numel() or own.dtype != flat.dtype:
+                    own = self._owned[t.name] = torch.empty_like(flat)
+                own.copy_(flat, non_blocking=True)
+                kept[t.name] = own
+        # owned buffers of tensors no longer in the checkpoint are released
+        for name in list(self._owned):
+            if name not in kept or kept[name] is not self._owned[name]:
+                del self._owned[name]
+        self.prev = (ckpt.iteration, kept)
 
     def _prev_map(self, ckpt, prev, kind):
         if kind not in (KIND_BASE, KIND_DELTA):
@@ -591,6 +631,15 @@ class CheckpointEncoder:
             pm = {t.name: t for t in prev.model_states}
         elif self.prev is not None:
             pm = dict(self.prev[1])
+            if self.keep_prev == "borrow":
+                for t in ckpt.model_states:
+                    b = pm.get(t.name)
+                    if (isinstance(t, DeviceTensor) and b is not None
+                            and _shares_storage(b, t.data)):
+                        raise StoreError(
+                            f"tensor {t.name!r}: the delta base borrowed at the previous save is "
+                            "the same device memory as the current state (mutated in place); "
+                            "use keep_prev='copy' or pass prev")
         else:
             raise MissingPreviousError(
                 f"delta save at iteration {ckpt.iteration} needs the previous "
@@ -598,6 +647,10 @@ class CheckpointEncoder:
         if set(pm) != {t.name for t in ckpt.model_states}:
             raise StoreError("model-state structure differs from previous checkpoint")
         return pm
+
+
+def _shares_storage(a: torch.Tensor, b: torch.Tensor) -> bool:
+    return a.untyped_storage().data_ptr() == b.untyped_storage().data_ptr()
 
 
 def blob_bound(ckpt: Checkpoint) -> int:
@@ -1237,3 +1290,10 @@ def write_tensors_bin(path: str, blob) -> None:
     """Byte sink of a store commit (store.py:350-351 writes tensors.bin)."""
     with open(path, "wb") as f:
         f.write(memoryview(blob.numpy() if isinstance(blob, torch.Tensor) else blob))
+
+
+# the reference store's file-system entry points around the codec
+# (store.py:84-111, 306-474), in fsstore.py
+from .fsstore import (MissingLinkError, StoreConfig, TrackerError, commit,  # noqa: E402
+                      decide_kind, list_iterations, load_checkpoint, read_manifest,
+                      read_tracker, save_checkpoint, try_read_tracker)

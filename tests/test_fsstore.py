@@ -1,0 +1,148 @@
+"""The reference store's save / load entry points over the B200 codec
+(fsstore.py; reference store.py:84-111, 306-474) and the async agent
+(engine.py:235-306): same on-disk layout, same tracker and base-refresh
+policy, byte-identical tensors.bin (the golden checkpoint the reference's own
+store wrote, tests/golden/make_golden.py)."""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+from paper_2511_12376_b200 import engine as E
+from paper_2511_12376_b200 import store as S
+from paper_2511_12376_b200.tensors import Checkpoint, ElementType, TensorBlob
+
+REF_SRC = "/root/reference/pkg/src"
+
+
+def _golden(g):
+    return [(S.CheckpointManifest.from_bytes(g[f"manifest{i}"].tobytes()), g[f"blob{i}"].tobytes())
+            for i in (0, 1)]
+
+
+def _golden_ckpts(g, meta):
+    model0, model1, opt = [], [], []
+    for name, shape in meta["shapes"].items():
+        shape = tuple(shape)
+        model0.append(TensorBlob(name, ElementType.F16, shape, g[f"w0:{name}"].astype("<u2").tobytes()))
+        model1.append(TensorBlob(name, ElementType.F16, shape, g[f"w1:{name}"].astype("<u2").tobytes()))
+        for kind in ("m", "v"):
+            opt.append(TensorBlob(f"adam.{kind}.{name}", ElementType.F32, shape,
+                                  g[f"{kind}:{name}"].astype("<f4").tobytes()))
+    return (Checkpoint(iteration=100, model_states=model0, optimizer_states=opt),
+            Checkpoint(iteration=110, model_states=model1, optimizer_states=opt))
+
+
+def test_commit_layout_and_policy(tmp_path, checkpoint_golden, monkeypatch):
+    monkeypatch.delenv("MAX_CACHED_ITERATION", raising=False)
+    cfg = S.StoreConfig(tmp_path / "store", max_cached_iteration=2)
+    assert S.decide_kind(cfg, 100) == S.KIND_BASE
+    (m0, b0), (m1, b1) = _golden(checkpoint_golden)
+    S.commit(cfg, m0, b0)
+    assert S.decide_kind(cfg, 110) == S.KIND_DELTA
+    S.commit(cfg, m1, b1)
+    assert S.decide_kind(cfg, 120) == S.KIND_BASE      # max_cached_iteration = 2
+    d = cfg.iter_dir(110)
+    assert d.name == "iter_0000110"
+    assert (d / "tensors.bin").read_bytes() == b1
+    assert (d / "manifest.bin").read_bytes() == m1.to_bytes()
+    assert (d / "type.txt").read_text() == "delta\n"
+    assert cfg.tracker_path().read_text() == "110\n100\n"
+    assert S.list_iterations(cfg) == [100, 110]
+    assert S.read_manifest(cfg, 110) == m1
+    with pytest.raises(S.MissingLinkError):
+        S.read_manifest(cfg, 105)
+    (cfg.root / ".needs_base").touch()
+    assert S.decide_kind(cfg, 120) == S.KIND_BASE
+    monkeypatch.setenv("MAX_CACHED_ITERATION", "5")
+    os.unlink(cfg.root / ".needs_base")
+    assert S.decide_kind(cfg, 120) == S.KIND_DELTA
+    with pytest.raises(S.StoreError):
+        S.StoreConfig(tmp_path / "x", redundancy_depth=0)
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_SRC), reason="reference not present (GPU box)")
+def test_reference_store_reads_our_commit(tmp_path, checkpoint_golden, golden_index):
+    """Interoperability: the reference's own load_checkpoint replays a store
+    our commit wrote (and our read_manifest reads the reference's)."""
+    sys.path.insert(0, REF_SRC)
+    try:
+        from bitsnap import store as RS
+    finally:
+        sys.path.remove(REF_SRC)
+    cfg = S.StoreConfig(tmp_path / "store", max_cached_iteration=2)
+    for m, b in _golden(checkpoint_golden):
+        S.commit(cfg, m, b)
+    out = RS.load_checkpoint(RS.StoreConfig(tmp_path / "store", max_cached_iteration=2))
+    _, c1 = _golden_ckpts(checkpoint_golden, golden_index["checkpoint"])
+    assert out.iteration == 110
+    assert [t.data for t in out.model_states] == [t.data for t in c1.model_states]
+    rcfg = RS.StoreConfig(tmp_path / "ref", max_cached_iteration=2)
+    (m0, b0), _ = _golden(checkpoint_golden)
+    RS.commit(rcfg, RS.CheckpointManifest.from_bytes(m0.to_bytes()), b0)
+    assert S.read_manifest(S.StoreConfig(tmp_path / "ref"), 100) == m0
+
+
+def test_async_agent_persists_staged_blobs(tmp_path, checkpoint_golden):
+    (m0, b0), (m1, b1) = _golden(checkpoint_golden)
+    region = E.SlotRegion.create(tmp_path / "r.bssl", ranks=2, redundancy=2,
+                                 capacity=len(b0) + 4096)
+    region.stage(0, S.pack_blob(m0, b0), 100)
+    region.stage(0, S.pack_blob(m1, b1), 110)
+    region.stage(1, S.pack_blob(m0, b0), 100)
+    agent = E.AsyncAgent(region, tmp_path / "stores", max_cached_iteration=2)
+    assert agent.persist_once() == 3
+    assert agent.errors == []
+    assert all(s.state == E.STATE_PERSISTED for s in region.all_slots() if s.iteration)
+    c0 = agent.rank_config(0)
+    assert (c0.iter_dir(110) / "tensors.bin").read_bytes() == b1
+    assert c0.tracker_path().read_text() == "110\n100\n"
+    assert (agent.rank_config(1).iter_dir(100) / "tensors.bin").read_bytes() == b0
+    # a corrupted slot stays VALID and is reported
+    region.stage(1, S.pack_blob(m1, b1), 110)
+    idx = [s.index for s in region.slots(1) if s.iteration == 110][0]
+    off = region._slot_offset(1, idx) + E.SLOT_HEADER.size + 100
+    region._mm[off] ^= 0xFF
+    assert agent.persist_once() == 0
+    assert "checksum mismatch" in agent.errors[-1]
+    agent.start()
+    agent.stop()
+    region.close()
+
+
+@pytest.mark.gpu
+def test_save_and_load_through_store(dev, tmp_path, checkpoint_golden, golden_index):
+    """save_checkpoint (GPU encode + commit) writes the reference store's
+    bytes; load_checkpoint replays the chain on the GPU."""
+    from oracle import bitsnap_oracle as O
+    c0, c1 = _golden_ckpts(checkpoint_golden, golden_index["checkpoint"])
+    (m0, b0), (m1, b1) = _golden(checkpoint_golden)
+    for use_encoder in (False, True):
+        root = tmp_path / f"s{int(use_encoder)}"
+        cfg = S.StoreConfig(root, max_cached_iteration=2)
+        enc = S.CheckpointEncoder(dev, clusters=16) if use_encoder else None
+        assert S.save_checkpoint(cfg, c0, None, encoder=enc) == m0
+        # with the resident encoder the delta needs no prev
+        assert S.save_checkpoint(cfg, c1, None if use_encoder else c0, encoder=enc) == m1
+        assert (cfg.iter_dir(100) / "tensors.bin").read_bytes() == b0
+        assert (cfg.iter_dir(110) / "tensors.bin").read_bytes() == b1
+        out = S.load_checkpoint(cfg)
+        assert out.iteration == 110
+        assert [t.data for t in out.model_states] == [t.data for t in c1.model_states]
+        for a, b in zip(out.optimizer_states, c1.optimizer_states):
+            x = np.frombuffer(b.data, np.float32)
+            tab = O.cluster_fit(x, 16)
+            p, c, _ = O.cluster_quantize(x, tab)
+            assert a.data == O.cluster_dequantize(p, c, x.size, tab).astype("<f4").tobytes()
+        assert [t.data for t in S.load_checkpoint(cfg, 100).model_states] == \
+            [t.data for t in c0.model_states]
+    # a failed delta save forces the next save to be a base (store.py:386-391)
+    cfg = S.StoreConfig(tmp_path / "fail", max_cached_iteration=3)
+    S.save_checkpoint(cfg, c0)
+    with pytest.raises(S.MissingPreviousError):
+        S.save_checkpoint(cfg, c1)          # delta without prev
+    assert (cfg.root / ".needs_base").exists()
+    assert S.save_checkpoint(cfg, c1).kind == S.KIND_BASE
+    assert not (cfg.root / ".needs_base").exists()

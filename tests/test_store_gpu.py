@@ -70,6 +70,49 @@ def test_resident_encoder_device_tensors(dev, checkpoint_golden, golden_index):
     assert man1.base_iteration == 100
 
 
+@pytest.mark.parametrize("graphs", ["1", "0"])
+def test_in_place_updates_between_saves(dev, checkpoint_golden, golden_index, monkeypatch,
+                                        graphs):
+    """A training loop saves its LIVE parameter buffers, which the optimizer
+    changes in place between saves: the resident delta base
+    must be the encoder's own copy, or every later delta would compare each
+    buffer with itself (n_c = 0) and a restore would give back the base."""
+    monkeypatch.setenv("BSNP_GRAPHS", graphs)
+    g, meta = checkpoint_golden, golden_index["checkpoint"]
+    c0, c1 = _golden_ckpts(g, meta)
+    live = [torch.from_numpy(np.frombuffer(t.data, np.int16).copy()).to(dev)
+            for t in c0.model_states]
+    opt = [S.DeviceTensor(t.name, t.dtype, t.shape,
+                          torch.from_numpy(np.frombuffer(t.data, np.float32).copy()).to(dev))
+           for t in c0.optimizer_states]
+
+    def snap(it):
+        return Checkpoint(iteration=it, optimizer_states=opt, model_states=[
+            S.DeviceTensor(t.name, t.dtype, t.shape, a) for t, a in zip(c0.model_states, live)])
+
+    enc = S.CheckpointEncoder(dev, clusters=16)
+    chain, states = [], []
+    rng = np.random.default_rng(3)
+    for it in range(4):
+        man, out = enc.encode(snap(100 + it), None, S.KIND_BASE if it == 0 else S.KIND_DELTA)
+        chain.append((man, out.numpy().tobytes()))
+        states.append([a.cpu().numpy().copy() for a in live])
+        for a in live:          # the optimizer step: in place
+            k = max(1, a.numel() // 50)
+            idx = torch.from_numpy(rng.choice(a.numel(), k, replace=False)).to(dev)
+            a.view(-1)[idx] += 1
+    for it in range(1, 4):
+        rec = S.decode_chain(chain[:it + 1])
+        for t, want in zip(rec.model_states, states[it]):
+            assert t.data == want.tobytes()
+        assert any(e.codec == S.CODEC_DELTA for e in chain[it][0].tensors)
+    # borrow mode refuses a base that is the same memory as the new state
+    enc_b = S.CheckpointEncoder(dev, clusters=16, keep_prev="borrow")
+    enc_b.encode(snap(200), None, S.KIND_BASE)
+    with pytest.raises(S.StoreError, match="mutated in place"):
+        enc_b.encode(snap(201), None, S.KIND_DELTA)
+
+
 def test_decode_chain_round_trip(dev, checkpoint_golden, golden_index):
     g, meta = checkpoint_golden, golden_index["checkpoint"]
     c0, c1 = _golden_ckpts(g, meta)

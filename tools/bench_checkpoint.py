@@ -201,7 +201,9 @@ def run_shard(args, rank: int, world: int):
     only, plan = shard_names(args.config, rank, world)
     c0, c1 = generate(args.config, dev, only=only)
     raw = sum(t.nbytes for t in c1.model_states + c1.optimizer_states)
-    enc = S.CheckpointEncoder(dev, clusters=16)
+    # c0 / c1 are immutable snapshot buffers: borrowed, not copied (a C4
+    # shard has no room for an owned copy of its weights)
+    enc = S.CheckpointEncoder(dev, clusters=16, keep_prev="borrow")
     import numpy as np
     from paper_2511_12376_b200 import _runtime as rt
 
