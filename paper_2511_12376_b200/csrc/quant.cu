@@ -986,6 +986,7 @@ __global__ void __launch_bounds__(kQThreads)
   }
 }
 
+#include "quant_stats.cuh"
 #include "quant_window.cuh"
 
 // ---------------------------------------------------------------- host plan
@@ -1036,6 +1037,9 @@ struct QWs {
   double* sd;        // nunits
   UGrid* ug;         // nunits
   uint32_t* need;    // nunits + 1: exact min/max round needed (per unit, any)
+  double* partials_q;   // total_tiles: sum (x - c)^2 per tile (quant_stats.cuh)
+  double* partials2_q;  // as partials2
+  uint32_t* list;       // 1 + nunits: units needing numpy's exact variance tree
   size_t bytes;
 };
 
@@ -1056,6 +1060,9 @@ QWs carve(const QPlan& P, void* ws) {
   w.sd = (double*)take(8 * (size_t)P.nunits);
   w.ug = (UGrid*)take(kUGridBytes * (size_t)P.nunits);
   w.need = (uint32_t*)take(4 * ((size_t)P.nunits + 1));
+  w.partials_q = (double*)take(8 * P.total_tiles);
+  w.partials2_q = (double*)take(8 * (size_t)P.nunits * (P.T_full >> kPreShift) + 8);
+  w.list = (uint32_t*)take(4 * ((size_t)P.nunits + 1));
   w.bytes = o;
   return w;
 }
@@ -1104,16 +1111,37 @@ bool window_enabled() {
   return on;
 }
 
+// BSNP_VAR_EXACT=1: every unit takes numpy's variance tree (tests of the
+// fallback path; read per call so a test can switch it)
+int var_exact_forced() {
+  const char* e = getenv("BSNP_VAR_EXACT");
+  return e && atoi(e) != 0;
+}
+
 int run_window(const float* x, const QPlan& P, bsnp_cluster_table* tables, uint8_t* labels,
                uint8_t* codes, const QWs& w, cudaStream_t s) {
   int rc;
   const unsigned tiles = (unsigned)P.total_tiles;
-  fit_tree_kernel<false><<<tiles, kQThreads, 0, s>>>(x, P, w.mu, w.partials);
-  if ((rc = launch_status("fit_tree_kernel<sum>"))) return rc;
-  if ((rc = launch_combine<false>(P, tables, w, s))) return rc;
-  fit_tree_kernel<true><<<tiles, kQThreads, 0, s>>>(x, P, w.mu, w.partials);
-  if ((rc = launch_status("fit_tree_kernel<var>"))) return rc;
-  if ((rc = launch_combine<true>(P, tables, w, s))) return rc;
+  // one read of x for mean and sigma (quant_stats.cuh); numpy's variance
+  // tree only for the units whose sigma interval does not decide the tables
+  fit_sum_kernel<<<tiles, kQThreads, 0, s>>>(x, P, w.partials, w.partials_q, w.list);
+  if ((rc = launch_status("fit_sum_kernel"))) return rc;
+  if (P.T_full > kPreGroup) {
+    pre_combine2_kernel<<<(unsigned)(2 * P.nunits * (P.T_full >> kPreShift)), kQThreads, 0, s>>>(
+        P, w.partials, w.partials_q, w.partials2, w.partials2_q);
+    if ((rc = launch_status("pre_combine2_kernel"))) return rc;
+  }
+  fit_stats_kernel<<<P.nunits, kQThreads, 0, s>>>(x, P, w.partials, w.partials_q, w.partials2,
+                                                   w.partials2_q, w.mu, w.fthr, tables, w.sd,
+                                                   w.list, var_exact_forced());
+  if ((rc = launch_status("fit_stats_kernel"))) return rc;
+  fit_var_fallback_kernel<<<(unsigned)std::min<uint64_t>(tiles, 2048), kQThreads, 0, s>>>(
+      x, P, w.mu, w.list, w.partials);
+  if ((rc = launch_status("fit_var_fallback_kernel"))) return rc;
+  fit_var_combine_kernel<<<std::min(P.nunits, 256u), kQThreads, 0, s>>>(P, w.partials, w.list,
+                                                                        w.mu, w.fthr, tables,
+                                                                        w.sd);
+  if ((rc = launch_status("fit_var_combine_kernel"))) return rc;
   fit_grid_kernel<<<P.nunits, kQThreads, 0, s>>>(P, w.mu, w.sd, w.ug, w.need + P.nunits);
   if ((rc = launch_status("fit_grid_kernel"))) return rc;
   const unsigned chunks = (unsigned)((uint64_t)(P.nunits - 1) * P.C_full + P.C_last);

@@ -364,3 +364,26 @@ def test_large_units_pre_reduced_combine(dev, n, block):
     x = (rng.standard_normal(n) * 1e-3).astype(np.float32)
     dq = Q.cluster_encode_device(_f32(x, dev), 16, block)
     _check_units(x, 16, block, dq)
+
+
+@pytest.mark.parametrize("n,block,dist,m", [
+    ((1 << 20) + 5, 0, "adam_m", 16), (100003, 8192, "adam_v", 7), (5 * 8192 + 100, 8192,
+                                                                     "offset", 16),
+    (3 * (1 << 16) + 1000, 1 << 16, "uniform", 2), ((1 << 24) + 12345, 0, "adam_v", 16),
+    (9 * 8192, 8192, "discrete", 16)])
+def test_exact_variance_fallback_vs_oracle(dev, monkeypatch, n, block, dist, m):
+    """The default fit reads x once: sigma comes from a rigorous interval
+    around numpy's variance (quant_stats.cuh), and only units whose f32
+    outputs the interval leaves undecided take numpy's variance tree.
+    BSNP_VAR_EXACT=1 sends every unit down that fallback: both paths must be
+    bit-exact vs the oracle and give identical bytes."""
+    from paper_2511_12376_b200 import quantizer as Q
+    rng = np.random.default_rng(n + m)
+    x = _dist(dist, n, rng).astype(np.float32)
+    xt = _f32(x, dev)
+    a = Q.cluster_encode_device(xt, m, block)
+    monkeypatch.setenv("BSNP_VAR_EXACT", "1")
+    b = Q.cluster_encode_device(xt, m, block)
+    _check_units(x, m, block, b)
+    for f in ("tables", "labels", "codes"):
+        assert bytes(getattr(a, f).cpu().numpy()) == bytes(getattr(b, f).cpu().numpy()), f
