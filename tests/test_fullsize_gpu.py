@@ -19,7 +19,7 @@ import numpy as np
 import pytest
 
 from oracle import bitsnap_oracle as O
-from tests import pool_oracle as PO
+import pool_oracle as PO
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
