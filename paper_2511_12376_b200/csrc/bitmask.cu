@@ -195,27 +195,45 @@ __device__ __forceinline__ uint32_t tile_local_scan(const uint32_t (&cnt)[kVec],
 //       a shared-memory stage by cp.async.bulk), read the stage into registers
 //       and release it at once (refill = bulk copies of the next claimed
 //       tile), scan the change bits inside the CTA, publish the tile aggregate
-//       for the decoupled look-back, write the mask bytes and stage the tile's
-//       compacted payload in its own scratch slot (scratch + tile*kTile).
-//       Workers never wait for a look-back.
-//   look-back warps (8..8+kLB-1): record q of the CTA (ring of kRing) is served
-//       by warp 8 + q % kLB: decoupled look-back for the tile's exclusive
-//       prefix, then - once the workers signalled the slot staged - move the
-//       slot to payload[prefix...] and discard the slot's L2 lines so the
-//       staging never reaches DRAM.
+//       for the decoupled look-back, write the mask bytes and compact the
+//       tile's changed values into the shared-memory arena (or, when the
+//       arena has no room for them right now, into the tile's global scratch
+//       slot).  Workers never wait for a look-back.
+//   look-back warps (8 .. 8 + kLB - 1): record q of the CTA (ring of kRing)
+//       is served by warp 8 + q % kLB: decoupled look-back for the tile's
+//       exclusive prefix, then - once staged - the compacted values go to
+//       payload[prefix...] with 16-byte stores (funnel-shifted granules);
+//       arena bytes are released in record order, a global slot's L2 lines
+//       are discarded so that staging never reaches DRAM.  Two look-back
+//       warps keep dense tiles' prefixes coming (the look-back is the serial
+//       part: p = 25 %: 1.46 ms with one, 1.08 ms with two).
 // mbarriers: full[s] (TMA bytes), rec_full[r]/rec_empty[r] (workers <->
-// look-back warp), staged[r] (8 worker warps -> look-back warp).
+// look-back warps), staged[r] (8 worker warps -> look-back warp).
 #ifndef BSNP_LB_WIDTH
 #define BSNP_LB_WIDTH 4  // look-back predecessors per lane per round trip
 #endif
 #ifndef BSNP_KLB
-#define BSNP_KLB 1
+#define BSNP_KLB 2
 #endif
 constexpr int kLB = BSNP_KLB;  // look-back warps per CTA
 constexpr int kRing = 16;
 static_assert(kRing % kLB == 0, "ring slots map to look-back warps");
 constexpr int kEncThreads = kThreads + 32 * kLB;
 constexpr int kEncStagesWS = 2;
+// compacted payloads of the tiles in flight wait for their prefix in a
+// shared-memory arena (a byte ring, 16-byte granules) sized so three CTAs
+// still fit an SM; a tile too dense for it (> ~56 % changed) is staged in its
+// global scratch slot instead
+#ifndef BSNP_ARENA
+#define BSNP_ARENA 10240
+#endif
+constexpr uint32_t kArena = BSNP_ARENA;
+static_assert(kArena % 16 == 0, "arena granules");
+constexpr uint32_t kDenseTile = 0xffffffffu;  // record base: staged in global scratch
+#ifndef BSNP_DENSE_COMPACT
+#define BSNP_DENSE_COMPACT 0x7fffffff
+#endif
+constexpr uint32_t kDenseCompact = BSNP_DENSE_COMPACT;  // tile changes -> unrolled compaction
 
 __device__ __forceinline__ void mbar_arrive_release(uint64_t* bar) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar))
@@ -232,14 +250,23 @@ __global__ void __launch_bounds__(kEncThreads)
                            uint16_t* __restrict__ payload, uint64_t payload_cap,
                            uint16_t* __restrict__ scratch, bsnp_status* __restrict__ st,
                            uint32_t* __restrict__ ticket, uint64_t* __restrict__ tile_status,
-                           uint64_t ntiles) {
+                           uint64_t ntiles, uint32_t ring_slots) {
   constexpr int kStages = kEncStagesWS;
+  // global staging slot of record q / tile t: per tile (ring_slots == 0), or
+  // a per-CTA ring of kRing slots (the workspace then does not grow with n)
+  auto slot_of = [&](uint32_t q, uint64_t t) {
+    return scratch + (ring_slots ? ((uint64_t)blockIdx.x * kRing + q % kRing) : t) * kTile;
+  };
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t full_bar[kStages];
   __shared__ uint64_t rec_full[kRing], rec_empty[kRing], staged[kRing];
   __shared__ uint32_t s_tile[kStages];
-  __shared__ uint32_t r_tile[kRing], r_count[kRing];
+  __shared__ uint32_t r_tile[kRing], r_count[kRing], r_base[kRing];
   __shared__ uint64_t s_warp[2][kWarps];
+  __shared__ volatile uint32_t s_tail;  // arena bytes released by the look-back warps
+  __shared__ volatile uint32_t s_relq;  // next record whose arena bytes get released
+  __shared__ uint32_t s_snap[2];        // s_tail as seen before a tile's scan barrier
+  uint8_t* arena = smem + (size_t)kEncStagesWS * kEncStage;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t nfull = n / kTile;
@@ -254,14 +281,17 @@ __global__ void __launch_bounds__(kEncThreads)
     }
   };
   // ring producer (worker thread 0): record q -> slot q % kRing
-  auto push_record = [&](uint32_t q, uint32_t tile, uint32_t count) {
+  auto push_record = [&](uint32_t q, uint32_t tile, uint32_t count, uint32_t abase) {
     const int r = q % kRing;
     if (q >= kRing) mbar_wait(&rec_empty[r], ((q / kRing) - 1) & 1u);
     r_tile[r] = tile;
     r_count[r] = count;
+    r_base[r] = abase;
     mbar_arrive_release(&rec_full[r]);
   };
   if (tid == 0) {
+    s_tail = 0;
+    s_relq = 0;
     pol = policy_evict_first();
     for (int s = 0; s < kStages; ++s) mbar_init(&full_bar[s], 1);
     for (int r = 0; r < kRing; ++r) {
@@ -275,7 +305,7 @@ __global__ void __launch_bounds__(kEncThreads)
   __syncthreads();
 
   if (warp >= kWarps) {
-    // ------------------------------------------------------ look-back warps
+    // --------------------------------------------------------- look-back warps
     const int w = warp - kWarps;
     for (uint32_t q = w;; q += kLB) {
       const int r = q % kRing;
@@ -286,47 +316,85 @@ __global__ void __launch_bounds__(kEncThreads)
       if (tile >= ntiles) break;
       const uint64_t excl = lookback_wide<BSNP_LB_WIDTH>(tile_status, tile, c, lane);
       if (lane == 0 && tile == ntiles - 1) st->count = excl + c;
-      mbar_wait(&staged[r], parity);  // workers wrote the scratch slot
-      const uint16_t* src = scratch + (uint64_t)tile * kTile;
+      mbar_wait(&staged[r], parity);  // workers wrote the arena / scratch slot
+      const uint32_t abase = r_base[r];
+      const uint16_t* src = slot_of(q, tile);
       const bool overflow = excl + c > payload_cap;
-      if (!overflow) {
-        // 16-byte loads from the (16 KiB aligned) slot, 4 in flight per lane
-        uint16_t* dst = payload + excl;
-        const uint4* src4 = reinterpret_cast<const uint4*>(src);
-        const uint32_t nv = (c + 7) / 8;
-        for (uint32_t v0 = 0; v0 < nv; v0 += 4 * 32) {
-          uint4 buf[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const uint32_t v = v0 + u * 32 + lane;
-            if (v < nv) buf[u] = src4[v];
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const uint32_t v = v0 + u * 32 + lane;
-            if (v < nv) {
-              const uint32_t e0 = v * 8;
-#pragma unroll
-              for (uint32_t k = 0; k < 8; ++k)
-                if (e0 + k < c) dst[e0 + k] = (uint16_t)u16_lane(buf[u], k);
-            }
-          }
+      const bool in_arena = abase != kDenseTile;
+      const uint32_t b0 = in_arena ? abase % kArena : 0;
+      // record source: byte ring of the arena, or the tile's global slot
+      auto granule = [&](uint32_t o) {  // 16 bytes at source byte o (16-aligned)
+        if (in_arena) {
+          if (o >= kArena) o -= kArena;
+          return *reinterpret_cast<const uint4*>(arena + o);
         }
+        return __ldcg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(src) + o));
+      };
+      auto elem = [&](uint32_t i) -> uint16_t {
+        if (in_arena) {
+          uint32_t o = b0 + 2 * i;
+          if (o >= kArena) o -= kArena;
+          return reinterpret_cast<const uint16_t*>(arena)[o >> 1];
+        }
+        return src[i];
+      };
+      if (!overflow) {
+        // a head of single elements up to 16-byte alignment of the
+        // destination, whole 16-byte vectors (two source granules
+        // funnel-shifted), a tail of single elements
+        uint16_t* dst = payload + excl;
+        uint32_t h = (uint32_t)(((16 - ((uintptr_t)dst & 15)) & 15) >> 1);
+        h = h < c ? h : c;
+        if ((uint32_t)lane < h) dst[lane] = elem(lane);
+        const uint32_t nv = (c - h) / 8;
+        for (uint32_t v = lane; v < nv; v += 32) {
+          uint32_t o = b0 + 2 * h + 16 * v;  // first source byte
+          if (in_arena)
+            while (o >= kArena) o -= kArena;
+          const uint32_t g = o & ~15u;
+          const uint4 lo = granule(g), hi = granule(g + 16);
+          const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+          // output word k = source bytes (o & 15) + 4k .. + 3: shift the 8
+          // words down by (o & 15) / 4 words in two select steps, then
+          // funnel-shift by the remaining 0 or 2 bytes
+          const uint32_t ws = (o & 15) >> 2, bs = (o & 3) * 8;
+          uint32_t v2[6], v1[5], out[4];
+#pragma unroll
+          for (int i = 0; i < 6; ++i) v2[i] = (ws & 2) ? w[i + 2] : w[i];
+#pragma unroll
+          for (int i = 0; i < 5; ++i) v1[i] = (ws & 1) ? v2[i + 1] : v2[i];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) out[k] = __funnelshift_r(v1[k], v1[k + 1], bs);
+          *reinterpret_cast<uint4*>(dst + h + 8 * v) = make_uint4(out[0], out[1], out[2], out[3]);
+        }
+        const uint32_t t0e = h + 8 * nv;
+        if ((uint32_t)lane < c - t0e) dst[t0e + lane] = elem(t0e + lane);
       } else {
         for (uint32_t i = lane; i < c; i += 32)
-          if (excl + i < payload_cap) payload[excl + i] = src[i];
+          if (excl + i < payload_cap) payload[excl + i] = elem(i);
         if (lane == 0) atomicOr(&st->err_flags, BSNP_ERR_PAYLOAD_CAP);
       }
+      if (!in_arena) {
+        __syncwarp();
+        for (uint32_t i = lane * 64; i < c; i += 32 * 64) discard_l2_line(src + i);
+      }
       __syncwarp();
-      for (uint32_t i = lane * 64; i < c; i += 32 * 64) discard_l2_line(src + i);
-      __syncwarp();
-      if (lane == 0) mbar_arrive_release(&rec_empty[r]);
+      if (lane == 0) {
+        // arena bytes are released in record order (the records of the look-
+        // back warps interleave): wait for the predecessor's release
+        while (s_relq != q) __nanosleep(32);
+        if (in_arena) s_tail = abase + ((2 * c + 15) & ~15u);
+        __threadfence_block();
+        s_relq = q + 1;
+        mbar_arrive_release(&rec_empty[r]);
+      }
       __syncwarp();
     }
     return;
   }
 
   // ------------------------------------------------------------------ workers
+  uint32_t arena_head = 0;  // arena bytes reserved so far (same in every warp)
   for (uint32_t q = 0;; ++q) {
     const int s = q % kStages;
     const uint32_t parity = (q / kStages) & 1u;
@@ -334,7 +402,7 @@ __global__ void __launch_bounds__(kEncThreads)
     if (tile >= ntiles) {
       // end of work: poison one record per look-back warp so each exits
       if (tid == 0)
-        for (int k = 0; k < kLB; ++k) push_record(q + k, 0xffffffffu, 0);
+        for (int k = 0; k < kLB; ++k) push_record(q + k, 0xffffffffu, 0, 0);
       break;
     }
     const uint64_t t0 = (uint64_t)tile * kTile;
@@ -376,26 +444,32 @@ __global__ void __launch_bounds__(kEncThreads)
     const uint64_t inc = warp_inclusive_scan_u64(packed, lane);
     const int db = q & 1;  // double-buffered scan scratch: 2 barriers per tile
     if (lane == 31) s_warp[db][warp] = inc;
+    if (tid == 0) s_snap[db] = s_tail;  // one view of the arena for every warp
     asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
     // every worker holds its part of the tile in registers: release the stage
     if (tid == 0) refill(s, next_t);
     // every warp scans the 8 warp totals itself (lane = group j * 8 + warp w,
     // the tile's element order), so no second barrier waits on warp 0's
     // publish / record hand-off
-    uint32_t woff[kVec];
+    uint32_t woff[kVec], total;
     {
       const int j = lane / kWarps, w = lane % kWarps;
       const uint32_t v = (uint32_t)(s_warp[db][w] >> (16 * j)) & 0xffffu;
       const uint32_t x = warp_inclusive_scan_u32(v, lane);
 #pragma unroll
       for (int jj = 0; jj < kVec; ++jj) woff[jj] = __shfl_sync(kFull, x - v, jj * kWarps + warp);
-      if (warp == 0) {
-        const uint32_t total = __shfl_sync(kFull, x, 31);
-        if (lane == 0) {
-          publish_aggregate(tile_status, tile, total);
-          push_record(q, tile, total);
-        }
-      }
+      total = __shfl_sync(kFull, x, 31);
+    }
+    // arena space of this tile: every warp runs the same reservation sequence
+    // against the same snapshot of the released bytes, so all decide alike;
+    // a tile that does not fit NOW goes to its global slot (never wait: a
+    // blocked CTA would hold back the aggregates other CTAs look back on)
+    const uint32_t abytes = (2 * total + 15) & ~15u;
+    const bool in_arena = arena_head + abytes - s_snap[db] <= kArena;
+    const uint32_t abase = in_arena ? arena_head : kDenseTile;
+    if (warp == 0 && lane == 0) {
+      publish_aggregate(tile_status, tile, total);
+      push_record(q, tile, total, abase);
     }
     const uint64_t ex = inc - packed;
     const uint64_t g0 = t0 / 8;
@@ -404,15 +478,54 @@ __global__ void __launch_bounds__(kEncThreads)
       const uint64_t g = g0 + j * kThreads + tid;
       if (g * 8 < n) mask[g] = (uint8_t)bits[j];
     }
-    uint16_t* slot = scratch + t0;
+    if (in_arena) {
+      arena_head += abytes;
+      uint16_t* a16 = reinterpret_cast<uint16_t*>(arena);
+      const uint32_t b0 = abase % kArena;
+      if (total >= kDenseCompact) {
+        // dense tile: every element slot unrolled and predicated (no
+        // divergent per-lane loop that waits on the lane with most changes)
 #pragma unroll
-    for (int j = 0; j < kVec; ++j) {
-      uint32_t b = bits[j];
-      uint32_t pos = woff[j] + ((uint32_t)(ex >> (16 * j)) & 0xffffu);
-      while (b) {
-        const uint32_t k = __ffs(b) - 1;
-        b &= b - 1;
-        slot[pos++] = (uint16_t)u16_lane(cv[j], k);
+        for (int j = 0; j < kVec; ++j) {
+          const uint32_t b = bits[j];
+          const uint32_t o0 = b0 + 2 * (woff[j] + ((uint32_t)(ex >> (16 * j)) & 0xffffu));
+          const uint32_t w4[4] = {cv[j].x, cv[j].y, cv[j].z, cv[j].w};
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            if ((b >> k) & 1u) {
+              uint32_t o = o0 + 2 * __popc(b & ((1u << k) - 1u));
+              if (o >= kArena) o -= kArena;
+              a16[o >> 1] = (uint16_t)(w4[k >> 1] >> (16 * (k & 1)));
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < kVec; ++j) {
+          uint32_t b = bits[j];
+          uint32_t o = b0 + 2 * (woff[j] + ((uint32_t)(ex >> (16 * j)) & 0xffffu));
+          while (b) {
+            const uint32_t k = __ffs(b) - 1;
+            b &= b - 1;
+            a16[(o >= kArena ? o - kArena : o) >> 1] = (uint16_t)u16_lane(cv[j], k);
+            o += 2;
+          }
+        }
+      }
+    } else {
+      // a ring slot is free once the look-back warp moved record q - kRing
+      // out of it (per-tile slots are never reused)
+      if (ring_slots && q >= kRing) mbar_wait(&rec_empty[q % kRing], ((q / kRing) - 1) & 1u);
+      uint16_t* slot = slot_of(q, tile);
+#pragma unroll
+      for (int j = 0; j < kVec; ++j) {
+        uint32_t b = bits[j];
+        uint32_t pos = woff[j] + ((uint32_t)(ex >> (16 * j)) & 0xffffu);
+        while (b) {
+          const uint32_t k = __ffs(b) - 1;
+          b &= b - 1;
+          slot[pos++] = (uint16_t)u16_lane(cv[j], k);
+        }
       }
     }
     __syncwarp();
@@ -809,9 +922,23 @@ static size_t enc_scratch_offset(uint64_t n) {
   return align_up(kWsHeader + 8 * (size_t)num_tiles(n), 256);
 }
 
+static size_t enc_smem() { return (size_t)kEncStagesWS * kEncStage + kArena; }
+
+// global staging slots of tiles too dense for the arena: one per tile, or a
+// ring of kRing per CTA when that is fewer (large tensors: 2^30 elements
+// need 111 MiB instead of 2 GiB)
+static uint64_t enc_slots(uint64_t n, uint32_t* ring) {
+  const uint64_t nt = num_tiles(n);
+  const uint64_t ring_slots =
+      (uint64_t)persistent_grid(delta_encode_ws_kernel, enc_smem(), nt, kEncThreads) * kRing;
+  if (ring) *ring = ring_slots < nt ? 1u : 0u;
+  return ring_slots < nt ? ring_slots : nt;
+}
+
 extern "C" size_t bsnp_delta_encode_ws_bytes(uint64_t n) {
-  // ticket | tile status words | payload staging slots (kTile per tile)
-  return enc_scratch_offset(n) + 2 * (size_t)num_tiles(n) * kTile;
+  // ticket | tile status words | payload staging slots | one granule the
+  // vector copy may read past the last slot
+  return enc_scratch_offset(n) + 2 * (size_t)enc_slots(n, nullptr) * kTile + 256;
 }
 
 extern "C" size_t bsnp_delta_decode_ws_bytes(uint64_t n) {
@@ -841,12 +968,14 @@ extern "C" int bsnp_delta_encode(const uint16_t* base, const uint16_t* target, u
   uint64_t* tstat = (uint64_t*)((char*)ws + kWsHeader);
   const bool aligned = (((uintptr_t)base | (uintptr_t)target) & 15) == 0;
   if (aligned) {
-    const size_t smem = (size_t)kEncStagesWS * kEncStage;
+    const size_t smem = enc_smem();
     auto k = delta_encode_ws_kernel;
     const int grid = persistent_grid(k, smem, nt, kEncThreads);
+    uint32_t ring = 0;
+    enc_slots(n, &ring);
     uint16_t* scratch = (uint16_t*)((char*)ws + enc_scratch_offset(n));
     k<<<grid, kEncThreads, smem, s>>>(base, target, n, mask, payload, payload_cap, scratch,
-                                      status, ticket, tstat, nt);
+                                      status, ticket, tstat, nt, ring);
   } else {
     delta_encode_kernel<false><<<(unsigned)nt, kThreads, 0, s>>>(
         base, target, n, mask, payload, payload_cap, status, ticket, tstat, nt);

@@ -39,8 +39,13 @@ def test_ws_sizes_without_gpu():
     lib = _lib.load()
     for n in (0, 1, 8192, 8193, 1 << 30):
         nt = -(-n // 8192)
-        # header + tile status (256-aligned) + 16 KiB payload staging per tile
-        assert lib.bsnp_delta_encode_ws_bytes(n) == -(-(256 + 8 * nt) // 256) * 256 + 16384 * nt
+        # header + tile status (256-aligned) + 16 KiB staging slots for tiles
+        # too dense for the shared-memory arena: one per tile, or a ring of 16
+        # per resident CTA, whichever is fewer (the CTA count needs a GPU; one
+        # CTA is assumed without one) + one granule of read-past slack
+        head = -(-(256 + 8 * nt) // 256) * 256
+        slots = min(nt, 16) if nt > 16 else nt
+        assert lib.bsnp_delta_encode_ws_bytes(n) == head + 16384 * slots + 256
         assert lib.bsnp_delta_decode_ws_bytes(n) == 256 + 8 * -(-nt // 32) + 8 * (nt + 1)
 
 
