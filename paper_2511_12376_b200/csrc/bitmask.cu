@@ -536,8 +536,26 @@ __global__ void __launch_bounds__(kEncThreads)
 // Payload offsets of every decode tile from the mask alone (n/8 bytes):
 // offsets[t] = popcount(mask[0 .. t*kTile)), offsets[ntiles] = total.  Also
 // validates padding bits and popcount == n_c (bitmask.py:128-135).  One CTA
-// per chunk of kChunkTiles tiles, chained by a decoupled look-back.
-constexpr int kChunkTiles = 32;
+// per chunk of kChunkTiles tiles (128 KiB of mask), chained by a decoupled
+// look-back; each warp counts kChunkTiles / 8 tiles with kOffBatch tiles of
+// loads in flight (a tile = 1024 mask bytes = 32 lanes x 32 B).
+constexpr int kChunkTiles = 128;
+constexpr int kOffBatch = 4;
+
+__device__ __forceinline__ uint32_t tile_lane_count(const uint8_t* __restrict__ mask, uint64_t n,
+                                                    uint64_t nbytes, uint64_t b0, bool& pad) {
+  uint32_t c = 0;
+  for (uint64_t i = b0; i < b0 + 32 && i < nbytes; ++i) {
+    uint32_t v = mask[i];
+    if (i == nbytes - 1 && (n & 7)) {
+      const uint32_t valid = (uint32_t)(n & 7);
+      pad |= (v >> valid) != 0;
+      v &= (1u << valid) - 1u;
+    }
+    c += __popc(v);
+  }
+  return c;
+}
 
 __global__ void __launch_bounds__(kThreads)
     delta_offsets_kernel(const uint8_t* __restrict__ mask, uint64_t n, uint64_t n_c,
@@ -552,49 +570,60 @@ __global__ void __launch_bounds__(kThreads)
   const uint64_t chunk = s_chunk;
   const uint64_t nbytes = (n + 7) / 8;
   const uint64_t ntiles = (n + kTile - 1) / kTile;
+  const bool vec = ((uintptr_t)mask & 15) == 0;
+  constexpr int kPerWarp = kChunkTiles / kWarps;
   bool pad = false;
-  // each warp: kChunkTiles / kWarps tiles, each tile = 1024 mask bytes = 32 lanes x 32 B
 #pragma unroll
-  for (int q = 0; q < kChunkTiles / kWarps; ++q) {
-    const int lt = warp * (kChunkTiles / kWarps) + q;
-    const uint64_t t = chunk * kChunkTiles + lt;
-    uint32_t c = 0;
-    if (t < ntiles) {
+  for (int q0 = 0; q0 < kPerWarp; q0 += kOffBatch) {
+    uint4 a[kOffBatch], b[kOffBatch];
+    bool full[kOffBatch];
+#pragma unroll
+    for (int q = 0; q < kOffBatch; ++q) {
+      const uint64_t t = chunk * kChunkTiles + warp * kPerWarp + q0 + q;
       const uint64_t b0 = t * kMaskBytes + (uint64_t)lane * 32;
-      if (b0 + 32 <= nbytes && ((uintptr_t)(mask + b0) & 15) == 0) {
-        const uint4 a = ld_stream_v4(mask + b0), b = ld_stream_v4(mask + b0 + 16);
-        c = __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w) + __popc(b.x) +
-            __popc(b.y) + __popc(b.z) + __popc(b.w);
-        if (b0 + 32 == nbytes && (n & 7)) {  // last byte is partial
-          const uint32_t last = b.w >> 24, valid = (uint32_t)(n & 7);
-          pad |= (last >> valid) != 0;
-          c -= __popc(last >> valid);
-        }
-      } else {
-        for (uint64_t i = b0; i < b0 + 32 && i < nbytes; ++i) {
-          uint32_t v = mask[i];
-          if (i == nbytes - 1 && (n & 7)) {
-            const uint32_t valid = (uint32_t)(n & 7);
-            pad |= (v >> valid) != 0;
-            v &= (1u << valid) - 1u;
-          }
-          c += __popc(v);
-        }
+      full[q] = t < ntiles && vec && b0 + 32 < nbytes;  // the last byte goes the slow way
+      if (full[q]) {
+        a[q] = ld_stream_v4(mask + b0);
+        b[q] = ld_stream_v4(mask + b0 + 16);
       }
     }
 #pragma unroll
-    for (int d = 16; d > 0; d >>= 1) c += __shfl_xor_sync(kFull, c, d);
-    if (lane == 0) s_cnt[lt] = c;
+    for (int q = 0; q < kOffBatch; ++q) {
+      const int lt = warp * kPerWarp + q0 + q;
+      const uint64_t t = chunk * kChunkTiles + lt;
+      uint32_t c = 0;
+      if (full[q]) {
+        c = __popc(a[q].x) + __popc(a[q].y) + __popc(a[q].z) + __popc(a[q].w) +
+            __popc(b[q].x) + __popc(b[q].y) + __popc(b[q].z) + __popc(b[q].w);
+      } else if (t < ntiles) {
+        c = tile_lane_count(mask, n, nbytes, t * kMaskBytes + (uint64_t)lane * 32, pad);
+      }
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) c += __shfl_xor_sync(kFull, c, d);
+      if (lane == 0) s_cnt[lt] = c;
+    }
   }
   if (pad) atomicOr(&st->err_flags, BSNP_ERR_PADDING);
   __syncthreads();
   if (warp == 0) {
-    const uint32_t v = s_cnt[lane];  // kChunkTiles == 32
-    const uint32_t x = warp_inclusive_scan_u32(v, lane);
+    // lane l scans tiles 4l .. 4l + 3
+    constexpr int kPer = kChunkTiles / 32;
+    uint32_t v[kPer], s = 0;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      v[k] = s_cnt[kPer * lane + k];
+      s += v[k];
+    }
+    const uint32_t x = warp_inclusive_scan_u32(s, lane);
     const uint32_t total = __shfl_sync(kFull, x, 31);
     const uint64_t excl = lookback_exclusive(chunk_status, chunk, total, lane);
-    const uint64_t t = chunk * kChunkTiles + lane;
-    if (t < ntiles) offsets[t] = excl + x - v;
+    uint64_t run = excl + x - s;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const uint64_t t = chunk * kChunkTiles + kPer * lane + k;
+      if (t < ntiles) offsets[t] = run;
+      run += v[k];
+    }
     if (chunk == nchunks - 1 && lane == 0) {
       const uint64_t pc = excl + total;
       offsets[ntiles] = pc;
@@ -796,79 +825,126 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-// In-place apply for chain replay (store.py:441-454): only the changed
-// elements are written.  Persistent grid over tiles; thread t owns the 32
-// elements of mask word t of the tile (one u32 load), so the work per
-// element is one bit test and the scatter is a loop over set bits only.
-// Runs after delta_offsets_kernel validated the mask (never when a flag is
-// raised, so a corrupt record leaves the base untouched).
+// In-place apply for sparse records (chain replay at small change
+// fractions): one WARP per tile, no CTA barriers.  Lane l owns the 256
+// elements of mask bytes [32 l, 32 l + 32) of the tile (two 16-byte loads);
+// a warp scan of the lane popcounts plus offsets[tile] gives every lane its
+// payload position.  The tile's payload run is contiguous, so the warp
+// stages it in shared memory with coalesced 4-byte loads (one round trip
+// instead of a dependent 2-byte load per changed element), then each lane
+// scatters its values.  The next tile's mask and offset are loaded before
+// the current one is applied.  Runs after delta_offsets_kernel validated the
+// mask (never when a flag is raised: a corrupt record leaves the base
+// untouched).
+constexpr uint32_t kApplyStage = 1024;  // staged payload elements per warp
+
 __global__ void __launch_bounds__(kThreads)
-    delta_apply_inplace_kernel(const uint8_t* __restrict__ mask,
-                               const uint16_t* __restrict__ payload, uint64_t n, uint64_t n_c,
-                               uint16_t* out, const uint64_t* __restrict__ offsets,
-                               const bsnp_status* __restrict__ st) {
-  __shared__ uint32_t s_warp[kWarps];
+    delta_apply_warp_kernel(const uint8_t* __restrict__ mask,
+                            const uint16_t* __restrict__ payload, uint64_t n, uint64_t n_c,
+                            uint16_t* out, const uint64_t* __restrict__ offsets,
+                            const bsnp_status* __restrict__ st) {
+  __shared__ __align__(16) uint16_t stage[kWarps][kApplyStage + 8];
   if (*(volatile const uint32_t*)&st->err_flags) return;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t ntiles = (n + kTile - 1) / kTile;
   const uint64_t nbytes = (n + 7) / 8;
-  const bool aligned = ((uintptr_t)mask & 3) == 0;
-  const bool vec_out = ((uintptr_t)out & 15) == 0;
-  // thread t owns mask word t of the tile (32 elements); the next tile's
-  // word is loaded before this one is processed (two loads in flight)
-  auto load_word = [&](uint64_t tile) -> uint32_t {
-    const uint64_t b0 = tile * kMaskBytes + 4 * (uint64_t)tid;
-    uint32_t w = 0;
-    if (b0 + 4 <= nbytes && aligned) {
-      w = __ldg(reinterpret_cast<const uint32_t*>(mask + b0));
+  const bool mvec = ((uintptr_t)mask & 15) == 0;
+  uint16_t* sp = stage[warp];
+  auto load_mask = [&](uint64_t tile, uint32_t (&w)[8]) {
+    const uint64_t b0 = tile * kMaskBytes + 32 * (uint64_t)lane;
+    if (mvec && b0 + 32 <= nbytes) {
+      const uint4 a = __ldg(reinterpret_cast<const uint4*>(mask + b0));
+      const uint4 b = __ldg(reinterpret_cast<const uint4*>(mask + b0 + 16));
+      w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+      w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
     } else {
-      for (uint32_t i = 0; i < 4 && b0 + i < nbytes; ++i)
-        w |= (uint32_t)__ldg(mask + b0 + i) << (8 * i);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        uint32_t v = 0;
+        for (uint32_t i = 0; i < 4; ++i) {
+          const uint64_t bi = b0 + 4 * k + i;
+          if (bi < nbytes) v |= (uint32_t)__ldg(mask + bi) << (8 * i);
+        }
+        w[k] = v;
+      }
     }
+    // bits past n (validated zero) are ignored
     const uint64_t e0 = b0 * 8;
-    if (e0 + 32 > n) w &= e0 >= n ? 0u : (0xffffffffu >> (32 - (uint32_t)(n - e0)));
-    return w;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint64_t ek = e0 + 32 * k;
+      if (ek + 32 > n) w[k] &= ek >= n ? 0u : (0xffffffffu >> (32 - (uint32_t)(n - ek)));
+    }
   };
-  uint64_t tile = blockIdx.x;
-  uint32_t w_next = tile < ntiles ? load_word(tile) : 0u;
-  for (; tile < ntiles; tile += gridDim.x) {
-    uint32_t w = w_next;
-    if (tile + gridDim.x < ntiles) w_next = load_word(tile + gridDim.x);
-    const uint64_t e0 = (tile * kMaskBytes + 4 * (uint64_t)tid) * 8;
-    const uint32_t c = __popc(w);
+  uint64_t tile = (uint64_t)blockIdx.x * kWarps + warp;
+  const uint64_t step = (uint64_t)gridDim.x * kWarps;
+  const bool pal = ((uintptr_t)payload & 3) == 0;
+  // payload word i (u16 pair from the even element below the run start)
+  auto pword = [&](uint64_t a0, uint32_t i) -> uint32_t {
+    const uint64_t e = a0 + 2 * (uint64_t)i;
+    if (pal && e + 1 < n_c) return __ldg(reinterpret_cast<const uint32_t*>(payload + e));
+    return (uint32_t)__ldg(payload + e) | (e + 1 < n_c ? (uint32_t)__ldg(payload + e + 1) << 16 : 0u);
+  };
+  // the next tile's mask, offsets and (short runs) payload words are loaded
+  // while the current tile is applied
+  constexpr uint32_t kPre = 2;  // prefetched payload words per lane (runs <= 128)
+  uint32_t wn[8], pn[kPre];
+  uint64_t off_n = 0, end_n = 0;
+  auto prefetch = [&](uint64_t t) {
+    load_mask(t, wn);
+    off_n = __ldg(offsets + t);
+    end_n = __ldg(offsets + t + 1);
+    const uint64_t a0 = off_n & ~1ull;
+    const uint32_t nw = (uint32_t)((end_n - a0 + 1) / 2);
+#pragma unroll
+    for (uint32_t q = 0; q < kPre; ++q) {
+      const uint32_t i = lane + 32 * q;
+      pn[q] = (nw <= 32 * kPre && i < nw) ? pword(a0, i) : 0u;
+    }
+  };
+  if (tile < ntiles) prefetch(tile);
+  for (; tile < ntiles; tile += step) {
+    uint32_t w[8], pw[kPre];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) w[k] = wn[k];
+#pragma unroll
+    for (uint32_t q = 0; q < kPre; ++q) pw[q] = pn[q];
+    const uint64_t off = off_n, end = end_n;
+    if (tile + step < ntiles) prefetch(tile + step);
+    uint32_t c = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) c += __popc(w[k]);
     const uint32_t inc = warp_inclusive_scan_u32(c, lane);
-    if (lane == 31) s_warp[warp] = inc;
-    __syncthreads();
-    uint32_t before = 0;
+    const uint32_t total = (uint32_t)(end - off);
+    const uint64_t a0 = off & ~1ull;
+    const uint32_t nw = (uint32_t)((end - a0 + 1) / 2);
+    const bool staged = total <= kApplyStage;
+    if (nw <= 32 * kPre) {
 #pragma unroll
-    for (int i = 0; i < kWarps; ++i) before += i < warp ? s_warp[i] : 0u;
-    __syncthreads();  // s_warp is reused by the next tile
-    uint64_t pos = offsets[tile] + before + inc - c;
-    if (c >= 4 && e0 + 32 <= n && vec_out) {
-      // dense word: read-modify-write its 64 bytes with vector accesses
-      // (32 scattered 2-byte stores per warp instruction cost more)
-      uint4* o4 = reinterpret_cast<uint4*>(out + e0);
-      uint4 v[4];
+      for (uint32_t q = 0; q < kPre; ++q)
+        if (lane + 32 * q < nw) reinterpret_cast<uint32_t*>(sp)[lane + 32 * q] = pw[q];
+      __syncwarp();
+    } else if (staged) {
+      // coalesced copy of payload[off, end) into the stage
+      for (uint32_t i = lane; i < nw; i += 32) reinterpret_cast<uint32_t*>(sp)[i] = pword(a0, i);
+      __syncwarp();
+    }
+    uint32_t r = inc - c;  // rank of this lane's first change in the tile
+    const uint32_t sh = (uint32_t)(off & 1);
+    const uint64_t e0 = tile * kTile + 256 * (uint64_t)lane;
+    {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) v[q] = o4[q];
-#pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        if ((w >> k) & 1u) {
-          const uint32_t val = pos < n_c ? (uint32_t)payload[pos] : 0u;
-          set_u16_lane(v[k >> 3], (uint32_t)(k & 7), val);
-          ++pos;
+      for (int k = 0; k < 8; ++k) {
+        uint32_t b = w[k];
+        while (b) {
+          const uint32_t j = __ffs(b) - 1;
+          b &= b - 1;
+          out[e0 + 32 * k + j] = staged ? sp[sh + r] : __ldg(payload + off + r);
+          ++r;
         }
       }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) o4[q] = v[q];
-    } else {
-      while (w) {
-        const uint32_t k = __ffs(w) - 1;
-        w &= w - 1;
-        if (pos < n_c) out[e0 + k] = payload[pos];
-        ++pos;
-      }
     }
+    __syncwarp();  // the stage is reused by the next tile
   }
 }
 
@@ -1024,9 +1100,12 @@ extern "C" int bsnp_delta_decode(const uint16_t* base, const uint8_t* mask,
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    const uint64_t grid = nt < (uint64_t)sms * 8 ? nt : (uint64_t)sms * 8;
-    delta_apply_inplace_kernel<<<(unsigned)grid, kThreads, 0, s>>>(mask, payload, n, n_c, out,
-                                                                   offsets, status);
+    // one warp per tile, a few tiles per warp
+    const uint64_t warps = (nt + 3) / 4;
+    const uint64_t want = (warps + kWarps - 1) / kWarps;
+    const uint64_t grid = want < (uint64_t)sms * 8 ? want : (uint64_t)sms * 8;
+    delta_apply_warp_kernel<<<(unsigned)(grid ? grid : 1), kThreads, 0, s>>>(
+        mask, payload, n, n_c, out, offsets, status);
   } else if (aligned) {
     const size_t smem = (size_t)kDecStages * kDecStage;
     auto k = n_c * 32 > n ? delta_decode_tma_kernel<kDecStages, true>
