@@ -54,7 +54,23 @@ def parse_args():
                     help="skip the whole-checkpoint line (BASELINE configs[0], GPT-2-small)")
     ap.add_argument("--c2-log2n", type=int, default=30)
     ap.add_argument("--c2-block", type=int, default=1 << 20)
+    ap.add_argument("--no-sweep", action="store_true",
+                    help="skip the C1 change-fraction sweep (p = 0.1 / 1 / 6.25 / 25 %%)")
+    ap.add_argument("--no-ckpt", action="store_true",
+                    help="skip the sharded whole-checkpoint line (planner over all ranks)")
+    ap.add_argument("--ckpt-config", default=None, choices=["C0", "C3", "C4"],
+                    help="checkpoint of the sharded line (default C3; C4 at 8 ranks)")
     return ap.parse_args()
+
+
+def max_over_ranks(values, dev):
+    """Element-wise max over the job (NCCL on device tensors, gloo on host)."""
+    import torch
+    import torch.distributed as dist
+    on = dev if dist.get_backend() == "nccl" else torch.device("cpu")
+    t = torch.tensor(values, dtype=torch.float64, device=on)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(v) for v in t.cpu().tolist()]
 
 
 def algo_bytes(n: int, n_c: int) -> tuple[int, int]:
@@ -183,6 +199,113 @@ def cpu_baseline(p: float, per_core: int, cores: int | None = None, reps: int = 
                       f"numpy oracle encode+decode, best of {reps}; cpu: {model}"}
 
 
+def _cpu_model():
+    try:
+        return [l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo")
+                if l.startswith("model name")][0]
+    except Exception:
+        return "unknown"
+
+
+def _c2_cpu_worker(args):
+    seed, block, blocks, dist, barrier = args
+    import numpy as np
+    from oracle import bitsnap_oracle as O
+    rng = np.random.default_rng(seed)
+    xs = []
+    for _ in range(blocks):
+        x = rng.standard_normal(block, dtype=np.float32) * np.float32(1e-3)
+        xs.append(x * x if dist == "adam_v" else x)
+    barrier.wait()
+    t0 = time.perf_counter()
+    for x in xs:
+        tab = O.cluster_fit(x, 16)
+        packed, codes, _ = O.cluster_quantize(x, tab)
+        O.cluster_dequantize(packed, codes, x.size, tab)
+    return len(xs) * block, time.perf_counter() - t0, t0
+
+
+def cpu_baseline_c2(block: int = 1 << 20, blocks_per_core: int = 2, cores: int | None = None,
+                    dist: str = "adam_m"):
+    """the reference's per-block cluster codec (oracle port:
+    build_clusters + quantize + dequantize, quantizer.py:100-204) on whole
+    2^20-element blocks, one process per core."""
+    import multiprocessing as mp
+    cores = cores or len(os.sched_getaffinity(0))
+    ctx = mp.get_context("fork")
+    with ctx.Manager() as mgr:
+        barrier = mgr.Barrier(cores)
+        with ctx.Pool(cores) as pool:
+            res = pool.map(_c2_cpu_worker, [(100 + i, block, blocks_per_core, dist, barrier)
+                                            for i in range(cores)])
+    elems = sum(r[0] for r in res)
+    wall = max(r[2] + r[1] for r in res) - min(r[2] for r in res)
+    # encode + decode algorithmic bytes (5.5 B per element each way, SURVEY §8(d))
+    return {"value": round(2 * 5.5 * elems / wall / 1e9, 4), "unit": "GB/s", "cores": cores,
+            "kind": "port",
+            "sample": f"{cores} x {blocks_per_core} blocks of {block} fp32 ({dist}), m = 16, "
+                      f"numpy oracle fit + quantize + dequantize; cpu: {_cpu_model()}"}
+
+
+def _c0_cpu_worker(args):
+    names, barrier = args
+    import numpy as np
+    from oracle import bitsnap_oracle as O
+    data = _C0_CPU["data"]
+    model = [(n, data[n][0].shape, 0, data[n][1]) for n in names]
+    prev = [(n, data[n][0].shape, 0, data[n][0]) for n in names]
+    opt = [(k + n, data[n][2].shape, 1, data[n][2 + i]) for n in names
+           for i, k in enumerate(("adam.m.", "adam.v."))]
+    barrier.wait()
+    t0 = time.perf_counter()
+    O.encode_checkpoint(model, opt, prev, "delta", 16)
+    return sum(10 * data[n][0].size for n in names), time.perf_counter() - t0, t0
+
+
+_C0_CPU: dict = {}
+
+
+def cpu_baseline_c0(cores: int | None = None, max_elems: int | None = None):
+    """the reference's whole-checkpoint encode (oracle port of
+    store.encode_checkpoint, store.py:214-272) on the C0 delta pair, tensors
+    spread over the cores (LPT); `max_elems` bounds the sample (1-core)."""
+    import multiprocessing as mp
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from bench_checkpoint import generate_cpu_recipe_host
+    data = generate_cpu_recipe_host("C0")
+    names = list(data)
+    if max_elems:
+        picked, tot = [], 0
+        for nm in names:
+            if tot + data[nm][0].size > max_elems and picked:
+                continue
+            picked.append(nm)
+            tot += data[nm][0].size
+        names = picked
+    _C0_CPU["data"] = data
+    cores = cores or len(os.sched_getaffinity(0))
+    bins = [[] for _ in range(cores)]
+    loads = [0] * cores
+    for nm in sorted(names, key=lambda k: -data[k][0].size):
+        i = loads.index(min(loads))
+        bins[i].append(nm)
+        loads[i] += data[nm][0].size
+    bins = [b for b in bins if b]
+    ctx = mp.get_context("fork")
+    with ctx.Manager() as mgr:
+        barrier = mgr.Barrier(len(bins))
+        with ctx.Pool(len(bins)) as pool:
+            res = pool.map(_c0_cpu_worker, [(b, barrier) for b in bins])
+    _C0_CPU.clear()
+    raw = sum(r[0] for r in res)
+    wall = max(r[2] + r[1] for r in res) - min(r[2] for r in res)
+    return {"value": round(raw / wall / 1e9, 4), "unit": "GB/s (raw checkpoint bytes / s)",
+            "cores": len(bins), "kind": "port",
+            "sample": f"{len(names)} of the C0 delta pair's tensors ({raw / 1e9:.3f} GB raw), "
+                      f"numpy oracle encode_checkpoint(kind=delta); cpu: {_cpu_model()}"}
+
+
 def run_reference(args, rank: int, world: int):
     if rank != 0:
         return
@@ -284,9 +407,7 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     enc_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
     dec_ms = sum(e[2].elapsed_time(e[3]) for e in evs) / args.steps
     if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms, = max_over_ranks([ms], dev)
         dist.barrier()
 
     eb, db = algo_bytes(n, k)
@@ -297,8 +418,14 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     if not args.no_e2e:
         e2e = run_e2e(args, base, cur, k, dev, world)
     del base, cur, mask, payload, out
+    sweep = None if args.no_sweep else run_c1_sweep(args, dev, world)
     c2 = None if args.no_c2 else run_c2(args, dev, world)
+    c2_modes = None if args.no_c2 else run_c2_modes(args, dev, world)
     c0 = None if (args.no_c0 or world > 1) else run_c0(dev)
+    ckpt = None
+    if not args.no_ckpt:
+        cfg = args.ckpt_config or ("C4" if world == 8 else "C3")
+        ckpt = run_ckpt_sharded(cfg, dev, rank, world)
 
     if rank != 0:
         return
@@ -331,29 +458,47 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     }
     if e2e:
         line["e2e"] = e2e
+    if sweep:
+        line["c1_sweep"] = sweep
     if c2:
         line["c2_cluster_quant"] = c2
+    if c2_modes:
+        line["c2_modes"] = c2_modes
     if c0:
         line["c0_checkpoint"] = c0
+    if ckpt:
+        line[ckpt.pop("key")] = ckpt
     if world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(args.p, args.cpu_elems_per_core)
         # the 1-core figure beside the all-core one
         one = cpu_baseline(args.p, args.cpu_elems_per_core, cores=1)
         line["cpu_baseline"]["value_1core"] = one["value"]
+        if not args.no_c2:
+            c2cpu = cpu_baseline_c2()
+            c2cpu["value_1core"] = cpu_baseline_c2(blocks_per_core=2, cores=1)["value"]
+            line["cpu_baseline_c2"] = c2cpu
+        if not args.no_c0:
+            c0cpu = cpu_baseline_c0()
+            c0cpu["value_1core"] = cpu_baseline_c0(cores=1, max_elems=3_000_000)["value"]
+            line["cpu_baseline_c0"] = c0cpu
     print(json.dumps(line), flush=True)
 
 
 def run_c0(dev, reps: int = 3):
     """BASELINE configs[0]: a GPT-2-small checkpoint pair (bf16 weights, fp32
-    Adam m/v; tools/bench_checkpoint.py recipe) saved as base + delta through
-    store.CheckpointEncoder into reused pinned buffers and restored with
-    decode_chain (blobs H2D, chain replay, dequantize).  GB/s = raw bytes /
-    wall time per call (device work and PCIe copies inside)."""
+    Adam m/v) generated by SURVEY §8(d)'s CPU recipe — the inputs the
+    reference's own store encoded for tests/golden/c0_ratio.json — saved as
+    base + delta through store.CheckpointEncoder into reused pinned buffers
+    and restored with decode_chain (blobs H2D, chain replay, dequantize).
+    The delta blob must be the reference's byte for byte (size and sha256).
+    GB/s = raw bytes / wall time per call (device work and PCIe copies
+    inside)."""
+    import hashlib
     import torch
     sys.path.insert(0, os.path.join(ROOT, "tools"))
-    from bench_checkpoint import generate
+    from bench_checkpoint import generate_cpu_recipe
     from paper_2511_12376_b200 import store as S
-    c0, c1 = generate("C0", dev)
+    c0, c1 = generate_cpu_recipe("C0", dev)
     raw = sum(t.nbytes for t in c1.model_states + c1.optimizer_states)
     enc = S.CheckpointEncoder(dev, clusters=16)
     bufs = [torch.empty(S.blob_bound(c), dtype=torch.uint8, pin_memory=True) for c in (c0, c1)]
@@ -377,16 +522,266 @@ def run_c0(dev, reps: int = 3):
         for k, v in (("save_base_s", t[0][0]), ("save_delta_s", t[1][0]), ("load_s", tl)):
             best[k] = min(best.get(k, 1e9), v)
     blob = chain[1][1].numel()
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "c0_ratio.json")) as f:
+            ref = json.load(f)
+    except Exception:
+        ref = {}
+    digest = hashlib.sha256(chain[1][1].numpy().tobytes()).hexdigest()
     return {"workload": "C0: GPT-2-small checkpoint (124.4M params, 148 tensors; bf16 weights, "
                         "fp32 Adam m/v, m = 16), base + delta save, chain restore",
             "raw_bytes": raw, "delta_blob_bytes": blob,
             "compression_ratio": round(raw / blob, 4),
+            "reference": {"delta_blob_bytes": ref.get("delta_blob_bytes"),
+                          "ratio": round(ref["ratio"], 4) if ref else None,
+                          "blob_identical": digest == ref.get("blob_sha256"),
+                          "source": "reference store.encode_checkpoint on the same inputs "
+                                    "(tests/golden/make_c0_ratio.py)"},
             "save_delta_gbs": round(raw / best["save_delta_s"] / 1e9, 2),
             "save_base_gbs": round(raw / best["save_base_s"] / 1e9, 2),
             "load_gbs": round(raw / best["load_s"] / 1e9, 2),
             **{k: round(v, 4) for k, v in best.items()},
             "timing": "host wall clock per call, device-resident inputs, pinned host "
                       "outputs, best of 3 after one untimed pair"}
+
+
+def run_c1_sweep(args, dev, world, reps: int = 3):
+    """BASELINE configs[1] at every change fraction it names: encode, decode
+    (out of place) and the in-place apply of chain replay, CUDA events per
+    op, inputs resident in HBM (4 GiB >> L2)."""
+    import torch
+    from paper_2511_12376_b200 import bitmask as B
+    from paper_2511_12376_b200 import _runtime as rt
+    n = 1 << args.log2n
+    hbm, kind = peaks()
+    out = {}
+    for p in (0.001, 0.01, 0.0625, 0.25):
+        base, cur, k = make_c1(n, p, args.seed + 3, dev)
+        mask = torch.empty((n + 7) // 8, dtype=torch.uint8, device=dev)
+        pay = torch.empty(n, dtype=torch.int16, device=dev)
+        res = torch.empty_like(base)
+        work = base.clone()
+        st = rt.new_status(dev, 3)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        t = [0.0, 0.0, 0.0]
+        for r in range(reps + 1):
+            work.copy_(base)
+            torch.cuda.synchronize(dev)
+            ev[0].record()
+            B.encode_delta_async(base, cur, mask, pay, st[0])
+            ev[1].record()
+            B.decode_delta_async(base, mask, pay[:k], k, res, st[1])
+            ev[2].record()
+            B.decode_delta_async(work, mask, pay[:k], k, work, st[2])
+            ev[3].record()
+            torch.cuda.synchronize(dev)
+            if r:
+                for i in range(3):
+                    t[i] += ev[i].elapsed_time(ev[i + 1]) / reps
+        assert torch.equal(res, cur) and torch.equal(work, cur)
+        mb = (n + 7) // 8
+        nbytes = (4 * n + mb + 2 * k, mb + 2 * k + 4 * n, mb + 4 * k)
+        row = {"n_c": k, "compression_ratio": round(2 * n / B.delta_size_bytes(n, k), 4)}
+        for name, ms, b in zip(("encode", "decode", "apply_in_place"), t, nbytes):
+            row[name + "_ms"] = round(ms, 4)
+            row[name + "_gbs"] = round(b / (ms * 1e-3) / 1e9, 1)
+            row[name + "_frac"] = round(b / (ms * 1e-3) / 1e9 / hbm, 4)
+        out[f"p={p}"] = row
+        del base, cur, mask, pay, res, work
+    return {"workload": f"C1 sweep: 2^{args.log2n} bf16, p = 0.1 / 1 / 6.25 / 25 %",
+            "bytes": "encode 4n + n/8 + 2n_c; decode n/8 + 2n_c + 4n; in-place n/8 + 4n_c "
+                     "(SURVEY §8(d))", "peak": hbm, "peak_kind": kind, "points": out}
+
+
+def run_c2_modes(args, dev, world, reps: int = 3):
+    """BASELINE configs[2] in every form the bench quotes: Adam-m and Adam-v
+    (v = |N(0,1e-3)|^2, one-sided, heavy-tailed), per 2^20 block and per
+    tensor (the store's layout), m = 16; encode and dequantize."""
+    import torch
+    from paper_2511_12376_b200 import quantizer as Q
+    from paper_2511_12376_b200 import _runtime as rt
+    n, m = 1 << args.c2_log2n, 16
+    hbm, kind = peaks()
+    algo = 4 * n + n + (n + 1) // 2
+    out = {}
+    for dist in ("adam_m", "adam_v"):
+        g = torch.Generator(device=dev).manual_seed(args.seed + (7 if dist == "adam_m" else 8))
+        x = torch.randn(n, device=dev, generator=g) * 1e-3
+        if dist == "adam_v":
+            x.mul_(x)
+        for block in (args.c2_block, 0):
+            tables = Q.new_tables(n, block, dev)
+            labels = torch.empty(Q.unit_label_bytes(n, block), dtype=torch.uint8, device=dev)
+            codes = torch.empty(n, dtype=torch.uint8, device=dev)
+            res = torch.empty_like(x)
+            st = rt.new_status(dev)
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            te = td = 0.0
+            for r in range(reps + 1):
+                ev[0].record()
+                Q.cluster_encode_async(x, m, block, tables, labels, codes)
+                ev[1].record()
+                Q.cluster_dequantize_async(labels, codes, n, block, tables, res, st)
+                ev[2].record()
+                torch.cuda.synchronize(dev)
+                if r:
+                    te += ev[0].elapsed_time(ev[1]) / reps
+                    td += ev[1].elapsed_time(ev[2]) / reps
+            (maxlab, flags), = rt.read_status(st)
+            assert flags == 0 and maxlab < m
+            units = Q.num_units(n, block)
+            enc_bytes = Q.serialized_quant_size("t", 1, block or n, m) * units
+            out[f"{dist},block={block or 'tensor'}"] = {
+                "encode_ms": round(te, 4), "decode_ms": round(td, 4),
+                "encode_gbs": round(algo / (te * 1e-3) / 1e9, 1),
+                "decode_gbs": round(algo / (td * 1e-3) / 1e9, 1),
+                "encode_frac": round(algo / (te * 1e-3) / 1e9 / hbm, 4),
+                "decode_frac": round(algo / (td * 1e-3) / 1e9 / hbm, 4),
+                "compression_ratio": round(4 * n / enc_bytes, 4),
+                "max_abs_err": float((res - x).abs().max())}
+            del tables, labels, codes, res
+        del x
+    return {"workload": f"C2 modes: 2^{args.c2_log2n} fp32, m = 16", "algorithmic_bytes": algo,
+            "peak": hbm, "peak_kind": kind, "points": out}
+
+
+def run_ckpt_sharded(config, dev, rank, world, reps: int = 2):
+    """A whole checkpoint sharded over the job: every rank
+    generates ITS share of the planner's LPT plan (bf16 w0 / w1 and the fp32
+    optimizer states, tools/bench_checkpoint.py shapes), saves a base and a
+    delta with planner.encode_sharded (its own GPU's encode + ONE all-gather
+    of the size table) landing its records in pinned host memory at their
+    global offsets, and restores its share with decode_chain (bit-exact
+    check of the weights).  Box GB/s = the checkpoint's raw bytes / the
+    slowest rank's time (barrier to completion)."""
+    import torch
+    import torch.distributed as dist
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from bench_checkpoint import generate, shapes, shard_names
+    from paper_2511_12376_b200 import planner as PL
+    from paper_2511_12376_b200 import store as S
+    from paper_2511_12376_b200.tensors import ElementType
+    only, lplan = shard_names(config, rank, world)
+    torch.cuda.empty_cache()
+    c0, c1 = generate(config, dev, only=only)
+    # specs of the WHOLE checkpoint in checkpoint order; every state of a
+    # layer tensor goes to the rank the LPT plan gave the tensor
+    shp = shapes(config)
+    owner_of = dict(zip((nm for nm, _ in shp), lplan.owner))
+    numel = {nm: int(torch.Size(sz).numel()) for nm, sz in shp}
+    specs, owner = [], []
+    for nm, _ in shp:
+        specs.append(PL.TensorSpec(nm, "model", 2 * numel[nm]))
+        owner.append(owner_of[nm])
+    pre = ["master.", "adam.m.", "adam.v."] if config == "C3" else ["adam.m.", "adam.v."]
+    for nm, _ in shp:
+        for p in pre:
+            specs.append(PL.TensorSpec(p + nm, "optimizer", 4 * numel[nm]))
+            owner.append(owner_of[nm])
+    load = [0] * world
+    for sp, r in zip(specs, owner):
+        load[r] += sp.nbytes
+    plan = PL.ShardPlan(world=world, owner=tuple(owner), load=tuple(load))
+    raw_total = sum(sp.nbytes for sp in specs)
+    enc = S.CheckpointEncoder(dev, clusters=16, keep_prev="borrow")
+    loc0 = {t.name: t for t in list(c0.model_states) + list(c0.optimizer_states)}
+    loc1 = {t.name: t for t in list(c1.model_states) + list(c1.optimizer_states)}
+    prev = {t.name: t for t in c0.model_states}
+    mine = plan.local_ids(rank)
+    # any encoding fits: a model state at most raw, an fp32 optimizer state
+    # always quantized (1.5 B per element), plus headers (store.blob_bound)
+    bound = sum(sp.nbytes if sp.group == "model" else 3 * sp.nbytes // 8
+                for sp in (specs[i] for i in mine)) + 512 * (len(mine) + 1)
+    import numpy as np
+    from paper_2511_12376_b200 import _runtime as rt
+    host = [np.empty(bound, dtype=np.uint8) for _ in range(2)]
+    for a in host:   # page-locked by registration (the caching allocator rounds up to 2^k)
+        assert rt.lib().bsnp_host_register(a.ctypes.data, bound) == 0, "host register failed"
+    bufs = [torch.from_numpy(a) for a in host]
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def save(kind, local, it, buf):
+        res = PL.encode_sharded(specs, local, prev if kind == "delta" else None, kind, it,
+                                0, rank, world, enc, plan=plan, out=buf)
+        return res, res.local_offsets
+
+    times = {}
+    for _ in range(reps):
+        for key, kind, it, buf in (("save_base_s", "base", 0, bufs[0]),
+                                   ("save_delta_s", "delta", 1, bufs[1])):
+            barrier()
+            t0 = time.perf_counter()
+            r = save(kind, loc0 if kind == "base" else loc1, it, buf)
+            torch.cuda.synchronize(dev)
+            times[key] = min(times.get(key, 1e9), time.perf_counter() - t0)
+            if kind == "base":
+                rb = r
+            else:
+                rd = r
+    del r
+    # restore this rank's share: its records form a chain of local blobs
+    def local_link(res, offs, buf):
+        ents = tuple(S.ManifestEntry(rec.name, rec.group, rec.codec, o, rec.length)
+                     for rec, o in zip(res.records, offs))
+        man = S.CheckpointManifest(iteration=res.manifest.iteration, kind=res.manifest.kind,
+                                   base_iteration=res.manifest.base_iteration, tensors=ents)
+        return man, buf[:offs[-1]]
+    chain = [local_link(*rb, bufs[0]), local_link(*rd, bufs[1])]
+    # the restore needs the HBM the inputs hold (a C3 rank: 108 GB of states
+    # + 75 GB of dequantized optimizer states): keep only the weights to
+    # compare with
+    def digest(flat):  # position-weighted sum of the bit patterns (exact, in int64)
+        v = flat.reshape(-1).view(torch.int16).to(torch.int64)
+        i = torch.arange(v.numel(), device=v.device, dtype=torch.int64) % 1000003 + 1
+        return int(v.sum()), int(((v + 40000) * i).sum())
+
+    want = {t.name: digest(t.flat()) for t in c1.model_states}
+    del c0, c1, loc0, loc1, prev, enc
+    torch.cuda.empty_cache()
+    barrier()
+    t0 = time.perf_counter()
+    restored = S.decode_chain(chain, device=dev, to_host=False)
+    torch.cuda.synchronize(dev)
+    times["load_s"] = time.perf_counter() - t0
+    exact = all(digest(t.data) == want[t.name] for t in restored.model_states) and \
+        len(restored.model_states) == len(want)
+    blob = rd[1][-1] if rd[1] else 0
+    del restored, want, chain, rb, rd
+    torch.cuda.synchronize(dev)
+    for a in host:
+        rt.lib().bsnp_host_unregister(a.ctypes.data)
+    del bufs, host
+    stats = torch.tensor([times["save_base_s"], times["save_delta_s"], times["load_s"],
+                          float(blob), 0.0 if exact else 1.0], dtype=torch.float64)
+    if world > 1:
+        if dist.get_backend() == "nccl":
+            stats = stats.to(dev)
+        gathered = [torch.zeros_like(stats) for _ in range(world)]
+        dist.all_gather(gathered, stats)
+        stats_all = torch.stack([g.cpu() for g in gathered])
+    else:
+        stats_all = stats[None]
+    mx = stats_all.max(dim=0).values.tolist()
+    blob_total = int(stats_all[:, 3].sum())
+    return {"key": f"{config.lower()}_sharded",
+            "workload": f"{config} whole checkpoint sharded over {world} rank(s): base + delta "
+                        "save (planner.encode_sharded, one size-table all-gather, records landed "
+                        "in pinned host memory), restore of each rank's share (decode_chain)",
+            "ranks": world, "raw_bytes": raw_total, "delta_blob_bytes": blob_total,
+            "compression_ratio": round(raw_total / max(blob_total, 1), 4),
+            "plan_imbalance": round(plan.imbalance, 4),
+            "save_base_s": round(mx[0], 4), "save_delta_s": round(mx[1], 4),
+            "load_s": round(mx[2], 4),
+            "save_delta_box_gbs": round(raw_total / mx[1] / 1e9, 2),
+            "save_base_box_gbs": round(raw_total / mx[0] / 1e9, 2),
+            "load_box_gbs": round(raw_total / mx[2] / 1e9, 2),
+            "restored_bit_exact": mx[4] == 0.0,
+            "timing": "host wall clock per rank from a barrier, max over ranks; best of "
+                      f"{reps} saves, one restore"}
 
 
 def run_c2(args, dev, world):
@@ -430,9 +825,7 @@ def run_c2(args, dev, world):
     te /= args.steps
     td /= args.steps
     if world > 1:
-        t = torch.tensor([te, td], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        te, td = (float(v) for v in t.tolist())
+        te, td = max_over_ranks([te, td], dev)
     units = Q.num_units(n, block)
     algo = 4 * n + n + (n + 1) // 2            # read x, write codes + labels
     enc_bytes = Q.serialized_quant_size("t", 1, block, m) * units
@@ -486,9 +879,7 @@ def run_e2e(args, base, cur, k, dev, world):
     torch.cuda.synchronize(dev)
     dt = (time.perf_counter() - t0) / steps
     if world > 1:
-        t = torch.tensor([dt], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dt = float(t.item())
+        dt, = max_over_ranks([dt], dev)
     eb, db = algo_bytes(n, k)
     mask = (n + 7) // 8
     return {"value": round(world * (eb + db) / dt / 1e9, 2), "unit": "GB/s",

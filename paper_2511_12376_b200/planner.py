@@ -138,11 +138,13 @@ class ShardResult:
     records: list               # this rank's EncodedRecords
     offsets: list               # their global offsets in tensors.bin
     total_bytes: int            # length of the whole tensors.bin
+    local: object = None        # host buffer holding the records back to back (`out`)
+    local_offsets: list = None  # their offsets in `local` (+ the end)
 
 
 def encode_sharded(specs, local, prev_local, kind: str, iteration: int, base_iteration: int,
                    rank: int, world: int, encoder, group=None, device=None,
-                   plan: ShardPlan | None = None) -> ShardResult:
+                   plan: ShardPlan | None = None, out=None) -> ShardResult:
     """store.encode_checkpoint (store.py:214-272) across `world` ranks.
 
     specs: [TensorSpec] of the whole checkpoint in checkpoint order (model
@@ -155,6 +157,12 @@ def encode_sharded(specs, local, prev_local, kind: str, iteration: int, base_ite
     then derives the same manifest, whose offsets equal the single-process
     driver's, so the records written at their offsets form a byte-identical
     tensors.bin.
+
+    out: a pinned (or registered) host uint8 buffer large enough for any
+    encoding of this rank's tensors: the records are then encoded in groups
+    and land back to back in it while later groups are encoded (the device
+    arenas of a group or two at a time: a rank's share of a 7B-70B
+    checkpoint fits beside its inputs), before the size-table exchange.
     """
     from .store import CheckpointManifest, ManifestEntry
     if plan is None:
@@ -165,7 +173,11 @@ def encode_sharded(specs, local, prev_local, kind: str, iteration: int, base_ite
     if kind == "delta":
         prev_map = {specs[gid].name: prev_local[specs[gid].name]
                     for gid in mine if specs[gid].group == "model"}
-    recs, _ = encoder.encode_records(items, prev_map, kind) if items else ([], {})
+    local_offs = None
+    if out is not None and items and hasattr(encoder, "encode_groups"):
+        recs, local_offs, _ = encoder.encode_groups(items, prev_map, kind, out)
+    else:
+        recs, _ = encoder.encode_records(items, prev_map, kind) if items else ([], {})
     rows = [(r.gid, CODEC_CODES[r.codec], r.count, r.length) for r in recs]
     gathered = exchange_sizes(rows, world, plan.max_rows, group=group, device=device)
     table = global_offsets(gathered, len(specs))
@@ -175,7 +187,8 @@ def encode_sharded(specs, local, prev_local, kind: str, iteration: int, base_ite
     manifest = CheckpointManifest(iteration=iteration, kind=kind,
                                   base_iteration=base_iteration, tensors=entries)
     total = (table[-1][2] + table[-1][3]) if table else 0
-    return ShardResult(manifest, recs, [table[r.gid][2] for r in recs], total)
+    return ShardResult(manifest, recs, [table[r.gid][2] for r in recs], total,
+                       out if local_offs is not None else None, local_offs)
 
 
 def write_shard(path: str, res: ShardResult, device=None) -> int:
@@ -185,13 +198,16 @@ def write_shard(path: str, res: ShardResult, device=None) -> int:
     import os
     import torch
     from .store import sequential_offsets
-    local_offs = sequential_offsets(res.records)
-    buf = torch.empty(max(local_offs[-1], 1), dtype=torch.uint8,
-                      pin_memory=torch.cuda.is_available())
-    if res.records:
-        if device is None and torch.cuda.is_available():
-            device = torch.device("cuda", torch.cuda.current_device())
-        _place(res.records, local_offs, buf, device)
+    if res.local is not None:       # landed already (encode_sharded(out=...))
+        local_offs, buf = res.local_offsets, res.local
+    else:
+        local_offs = sequential_offsets(res.records)
+        buf = torch.empty(max(local_offs[-1], 1), dtype=torch.uint8,
+                          pin_memory=torch.cuda.is_available())
+        if res.records:
+            if device is None and torch.cuda.is_available():
+                device = torch.device("cuda", torch.cuda.current_device())
+            _place(res.records, local_offs, buf, device)
     fd = os.open(path, os.O_WRONLY | os.O_CREAT, 0o644)
     try:
         if os.fstat(fd).st_size < res.total_bytes:

@@ -217,6 +217,12 @@ class EncodedRecord:
     def length(self) -> int:
         return len(self.header) + sum(_part_nbytes(p) for p in self.parts)
 
+    def release(self) -> None:
+        """Drop the body parts once the record landed (they reference device
+        arenas); the length stays known."""
+        _ = self.length
+        self.parts = []
+
 
 def _part_nbytes(p) -> int:
     if isinstance(p, torch.Tensor):
@@ -532,7 +538,26 @@ class CheckpointEncoder:
         items = [(i, GROUP_MODEL, t) for i, t in enumerate(ckpt.model_states)]
         k = len(items)
         items += [(k + i, GROUP_OPTIMIZER, t) for i, t in enumerate(ckpt.optimizer_states)]
+        all_recs, offsets, model_dev = self.encode_groups(items, prev_map, kind, buf, ng)
+        base_iter = ckpt.iteration if kind == KIND_BASE else prev_iteration(prev, self.prev)
+        manifest = CheckpointManifest(
+            iteration=ckpt.iteration, kind=kind, base_iteration=base_iter,
+            tensors=tuple(ManifestEntry(r.name, r.group, r.codec, o, r.length)
+                          for r, o in zip(all_recs, offsets)))
+        self._retain(ckpt, model_dev)
+        return manifest, buf[:offsets[-1]]
+
+    def encode_groups(self, items, prev_map, kind: str, buf, ng: int | None = None):
+        """encode_records in ~ng groups of equal raw bytes, each group's
+        records landing at consecutive offsets of the pinned host buffer
+        `buf` (on a copy stream, while the next group is encoded), so the
+        device arenas of only a group or two are alive at a time.  Returns
+        (records, their offsets + the end offset, {name: device flat model
+        state}).  The shard planner lands a rank's records this way at
+        rank-local offsets before the size-table exchange."""
         total = sum(t.nbytes for _, _, t in items)
+        if ng is None:
+            ng = self._groups(total)
         groups, cur, acc = [], [], 0
         for it in items:
             cur.append(it)
@@ -545,7 +570,7 @@ class CheckpointEncoder:
         if not hasattr(self, "_copy_stream"):
             self._copy_stream = torch.cuda.Stream(self.dev)
         cs, main = self._copy_stream, torch.cuda.current_stream(self.dev)
-        all_recs, offsets, model_dev, keep = [], [0], {}, []
+        all_recs, offsets, model_dev, pending = [], [0], {}, []
         # graphs only for small checkpoints (a graph per group would pin its
         # arenas in memory)
         small = total <= GRAPH_MAX_ARENA
@@ -560,17 +585,23 @@ class CheckpointEncoder:
                 with torch.cuda.stream(cs):
                     tmp = place_records(recs, offs, buf[offs[0]:], self.dev, offs[0],
                                         sync=False)
-                keep.append((recs, tmp))  # arenas and staging live until the copies ran
+                    done = torch.cuda.Event()
+                    done.record(cs)
+                # a group's arenas and staging live until its copies ran; at
+                # most two groups' are kept (the oldest is long landed)
+                pending.append((done, recs, tmp))
+                while len(pending) > 2:
+                    ev, old_recs, _ = pending.pop(0)
+                    ev.synchronize()
+                    for r in old_recs:
+                        r.release()
                 all_recs += recs
                 offsets += offs[1:]
             cs.synchronize()
-        base_iter = ckpt.iteration if kind == KIND_BASE else prev_iteration(prev, self.prev)
-        manifest = CheckpointManifest(
-            iteration=ckpt.iteration, kind=kind, base_iteration=base_iter,
-            tensors=tuple(ManifestEntry(r.name, r.group, r.codec, o, r.length)
-                          for r, o in zip(all_recs, offsets)))
-        self._retain(ckpt, model_dev)
-        return manifest, buf[:offsets[-1]]
+            for _, old_recs, _ in pending:
+                for r in old_recs:
+                    r.release()
+        return all_recs, offsets, model_dev
 
     def encode_into(self, ckpt: Checkpoint, prev: Checkpoint | None, kind: str, dest):
         """encode() with the landing zone chosen once the sizes are known:

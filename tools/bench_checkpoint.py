@@ -105,6 +105,42 @@ def generate(config: str, dev, seed: int = 0, only=None):
             Checkpoint(iteration=1, model_states=cur, optimizer_states=opt))
 
 
+def generate_cpu_recipe_host(config: str, seed: int = 0) -> dict:
+    """SURVEY §8(d)'s C0 recipe exactly (the inputs of the reference's
+    published ratios, tests/golden/c0_ratio.json): ONE CPU torch.Generator
+    seeded 0; per tensor, in checkpoint order, w0 = randn * 0.02, u = randn,
+    w1 = w0 - 1e-5 u, m = randn * 1e-3, v = (randn * 1e-3)^2; weights saved as
+    bf16 (round to nearest even).  -> {name: (w0 u16, w1 u16, m f32, v f32)}"""
+    import torch
+    g = torch.Generator().manual_seed(seed)
+    out = {}
+    for name, shp in shapes(config):
+        w0 = torch.randn(shp, generator=g) * 0.02
+        u = torch.randn(shp, generator=g)
+        w1 = w0 - 1e-5 * u
+        m = torch.randn(shp, generator=g) * 1e-3
+        v = (torch.randn(shp, generator=g) * 1e-3) ** 2
+        b = lambda t: t.to(torch.bfloat16).view(torch.int16).numpy().view("<u2")
+        out[name] = (b(w0), b(w1), m.numpy(), v.numpy())
+    return out
+
+
+def generate_cpu_recipe(config: str, dev, seed: int = 0):
+    """generate_cpu_recipe_host, moved to the GPU as DeviceTensors."""
+    import torch
+    from paper_2511_12376_b200.store import DeviceTensor
+    from paper_2511_12376_b200.tensors import Checkpoint
+    base, cur, opt = [], [], []
+    for name, (w0, w1, m, v) in generate_cpu_recipe_host(config, seed).items():
+        bf = lambda a: torch.from_numpy(a.view("<i2")).to(dev).view(torch.bfloat16)
+        base.append(DeviceTensor.wrap(name, bf(w0)))
+        cur.append(DeviceTensor.wrap(name, bf(w1)))
+        opt.append(DeviceTensor.wrap("adam.m." + name, torch.from_numpy(m).to(dev)))
+        opt.append(DeviceTensor.wrap("adam.v." + name, torch.from_numpy(v).to(dev)))
+    return (Checkpoint(iteration=0, model_states=base, optimizer_states=opt),
+            Checkpoint(iteration=1, model_states=cur, optimizer_states=opt))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="C0", choices=["C0", "C3", "C4"])
