@@ -218,11 +218,15 @@ int bsnp_gather_segments(const bsnp_segment* segs, const uint32_t* first, uint32
 
 /*
  * Reduction behind precision_report (quantizer.py:280-296): acc3 receives
- * { sum (o-r)^2, sum |o-r|/|o| over |o| > 1e-12, count of |o| > 1e-12 } in
- * float64 (MSE = acc3[0]/n, MRE = acc3[1]/acc3[2]).
+ * (sum (o-r)^2, sum |o-r|/|o| over |o| > 1e-12, count of those o) in float64.
+ * Deterministic: a fixed partition of [0, n) into kPrecParts contiguous
+ * ranges (independent of the GPU), each reduced in a fixed order into the
+ * workspace, then one fixed tree over the partials - the same bits on every
+ * run.  ws: bsnp_precision_ws_bytes() bytes of device memory.
  */
+size_t bsnp_precision_ws_bytes(void);
 int bsnp_precision_report(const float* original, const float* restored, uint64_t n,
-                          double* acc3, void* stream);
+                          double* acc3, void* ws, size_t ws_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -35,7 +35,8 @@ SIGNATURES = {
     "bsnp_cluster_quantize": (_i32, [_vp, _u64, _u64, _vp, _vp, _vp, _vp, _sz, _vp]),
     "bsnp_cluster_encode": (_i32, [_vp, _u64, _u64, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
     "bsnp_cluster_dequantize": (_i32, [_vp, _vp, _u64, _u64, _vp, _vp, _vp, _vp, _sz, _vp]),
-    "bsnp_precision_report": (_i32, [_vp, _vp, _u64, _vp, _vp]),
+    "bsnp_precision_ws_bytes": (_sz, []),
+    "bsnp_precision_report": (_i32, [_vp, _vp, _u64, _vp, _vp, _sz, _vp]),
     "bsnp_gather_segments": (_i32, [_vp, _vp, _c.c_uint32, _c.c_uint32, _vp, _vp]),
     "bsnp_copy_sm": (_i32, [_vp, _vp, _u64, _vp]),
     "bsnp_cluster_dequantize_batch": (_i32, [_vp, _vp, _c.c_uint32, _c.c_uint32, _vp, _vp]),

@@ -958,13 +958,45 @@ __global__ void __launch_bounds__(kQThreads)
 }
 
 // ------------------------------------------------------- precision report
-// sum (o-r)^2, sum |o-r|/|o| over |o| > 1e-12, count of such o (float64)
+// sum (o-r)^2, sum |o-r|/|o| over |o| > 1e-12, count of such o (float64).
+// Deterministic: part p of kPrecParts reduces the contiguous range
+// [p n / P, (p + 1) n / P) - each thread a strided subsequence in order, then
+// a fixed shuffle / shared-memory tree - and one CTA folds the P partials in
+// a fixed tree.  No atomics: the same bits on every run and every GPU.
+constexpr int kPrecParts = 1024;
+
+__device__ __forceinline__ void block_sum3(double& a, double& b, double& c, double* sm) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    a += __shfl_xor_sync(kFull, a, d);
+    b += __shfl_xor_sync(kFull, b, d);
+    c += __shfl_xor_sync(kFull, c, d);
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (lane == 0) {
+    sm[3 * warp] = a;
+    sm[3 * warp + 1] = b;
+    sm[3 * warp + 2] = c;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    a = b = c = 0.0;
+    for (int w = 0; w < nw; ++w) {
+      a += sm[3 * w];
+      b += sm[3 * w + 1];
+      c += sm[3 * w + 2];
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kQThreads)
     precision_kernel(const float* __restrict__ o, const float* __restrict__ r, uint64_t n,
-                     double* __restrict__ acc) {
+                     double* __restrict__ parts) {
+  __shared__ double sm[3 * kQThreads / 32];
+  const uint64_t p = blockIdx.x;
+  const uint64_t lo = p * n / kPrecParts, hi = (p + 1) * n / kPrecParts;
   double sse = 0.0, rel = 0.0, cnt = 0.0;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x) {
+  for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
     const double a = (double)o[i], b = (double)r[i];
     const double e = a - b;
     sse += e * e;
@@ -973,16 +1005,28 @@ __global__ void __launch_bounds__(kQThreads)
       cnt += 1.0;
     }
   }
-#pragma unroll
-  for (int d = 16; d > 0; d >>= 1) {
-    sse += __shfl_xor_sync(kFull, sse, d);
-    rel += __shfl_xor_sync(kFull, rel, d);
-    cnt += __shfl_xor_sync(kFull, cnt, d);
+  block_sum3(sse, rel, cnt, sm);
+  if (threadIdx.x == 0) {
+    parts[3 * p] = sse;
+    parts[3 * p + 1] = rel;
+    parts[3 * p + 2] = cnt;
   }
-  if ((threadIdx.x & 31) == 0) {
-    atomicAdd(&acc[0], sse);
-    atomicAdd(&acc[1], rel);
-    atomicAdd(&acc[2], cnt);
+}
+
+__global__ void __launch_bounds__(kQThreads)
+    precision_final_kernel(const double* __restrict__ parts, double* __restrict__ acc) {
+  __shared__ double sm[3 * kQThreads / 32];
+  double a = 0.0, b = 0.0, c = 0.0;
+  for (int p = threadIdx.x; p < kPrecParts; p += blockDim.x) {
+    a += parts[3 * p];
+    b += parts[3 * p + 1];
+    c += parts[3 * p + 2];
+  }
+  block_sum3(a, b, c, sm);
+  if (threadIdx.x == 0) {
+    acc[0] = a;
+    acc[1] = b;
+    acc[2] = c;
   }
 }
 
@@ -1259,14 +1303,19 @@ extern "C" int bsnp_cluster_dequantize_batch(const bsnp_dequant_item* items,
   return launch_status("dequantize_batch_kernel");
 }
 
+extern "C" size_t bsnp_precision_ws_bytes(void) { return 3 * sizeof(double) * kPrecParts; }
+
 extern "C" int bsnp_precision_report(const float* original, const float* restored, uint64_t n,
-                                     double* acc3, void* stream) {
-  if (!acc3 || (n && (!original || !restored))) return BSNP_E_INVALID;
+                                     double* acc3, void* ws, size_t ws_bytes, void* stream) {
+  if (!acc3 || (n && (!original || !restored || !ws))) return BSNP_E_INVALID;
   cudaStream_t s = (cudaStream_t)stream;
-  int rc = cuda_status("memset(acc)", cudaMemsetAsync(acc3, 0, 3 * sizeof(double), s));
-  if (rc || n == 0) return rc;
-  uint64_t grid = (n + kQThreads - 1) / kQThreads;
-  if (grid > 148 * 8) grid = 148 * 8;
-  precision_kernel<<<(unsigned)grid, kQThreads, 0, s>>>(original, restored, n, acc3);
-  return launch_status("precision_kernel");
+  if (n == 0)
+    return cuda_status("memset(acc)", cudaMemsetAsync(acc3, 0, 3 * sizeof(double), s));
+  if (ws_bytes < bsnp_precision_ws_bytes()) return BSNP_E_WORKSPACE;
+  double* parts = (double*)ws;
+  precision_kernel<<<kPrecParts, kQThreads, 0, s>>>(original, restored, n, parts);
+  int rc = launch_status("precision_kernel");
+  if (rc) return rc;
+  precision_final_kernel<<<1, kQThreads, 0, s>>>(parts, acc3);
+  return launch_status("precision_final_kernel");
 }

@@ -19,8 +19,10 @@ def precision_device(original: torch.Tensor, restored: torch.Tensor) -> dict:
     if o.dtype != torch.float32 or r.dtype != torch.float32 or o.numel() != r.numel():
         raise ValueError("precision_device needs two float32 tensors of equal size")
     acc = torch.empty(3, dtype=torch.float64, device=o.device)
-    _lib.check(rt.lib().bsnp_precision_report(o.data_ptr(), r.data_ptr(), o.numel(),
-                                              acc.data_ptr(), rt.stream_ptr(o.device)),
+    lib = rt.lib()
+    ws = rt.workspace(o.device, lib.bsnp_precision_ws_bytes(), "prec")
+    _lib.check(lib.bsnp_precision_report(o.data_ptr(), r.data_ptr(), o.numel(), acc.data_ptr(),
+                                         ws.data_ptr(), ws.numel(), rt.stream_ptr(o.device)),
                "bsnp_precision_report")
     sse, rel, cnt = acc.cpu().tolist()
     n = o.numel()

@@ -387,3 +387,19 @@ def test_exact_variance_fallback_vs_oracle(dev, monkeypatch, n, block, dist, m):
     _check_units(x, m, block, b)
     for f in ("tables", "labels", "codes"):
         assert bytes(getattr(a, f).cpu().numpy()) == bytes(getattr(b, f).cpu().numpy()), f
+
+
+def test_precision_report_deterministic(dev):
+    """The float64 reduction has a fixed order (no atomics): the same bits on
+    every run (quantizer.py:280-296 semantics, rel 1e-9 of numpy's order)."""
+    import torch
+    from paper_2511_12376_b200.metrics import precision_device
+    g = torch.Generator(device=dev).manual_seed(4)
+    x = torch.randn((1 << 24) + 77, device=dev, generator=g)
+    y = x + torch.randn(x.numel(), device=dev, generator=g) * 1e-4
+    x[::1000] = 0.0
+    reps = [precision_device(x, y) for _ in range(5)]
+    assert all(r == reps[0] for r in reps)
+    want = O.precision(x.cpu().numpy(), y.cpu().numpy())
+    assert reps[0]["mse"] == pytest.approx(want["mse"], rel=1e-9)
+    assert reps[0]["mre"] == pytest.approx(want["mre"], rel=1e-9)
