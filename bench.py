@@ -162,12 +162,13 @@ def _cpu_worker(args):
     k = int(round(p * n))
     idx = rng.choice(n, k, replace=False)
     cur[idx] += 1
+    bb, cb = base.tobytes(), cur.tobytes()   # TensorBlob.data, as the reference holds it
     barrier.wait()
     t0 = time.perf_counter()
-    mask, payload, n_c = O.delta_encode(base, cur)
-    out = O.delta_decode(base, mask, payload, n, n_c)
+    mask, payload, n_c = O.ref_encode_bytes(bb, cb)
+    out = O.ref_decode_bytes(bb, mask, payload, n, n_c)
     dt = time.perf_counter() - t0
-    assert out[idx[0]] == cur[idx[0]]
+    assert out == cb
     e, d = algo_bytes(n, n_c)
     return e + d, dt, t0
 
@@ -196,7 +197,9 @@ def cpu_baseline(p: float, per_core: int, cores: int | None = None, reps: int = 
     return {"value": round(best, 3), "unit": "GB/s", "cores": cores,
             "kind": "port",
             "sample": f"{cores} x {per_core} bf16 elements (one per core), p={p}, "
-                      f"numpy oracle encode+decode, best of {reps}; cpu: {model}"}
+                      f"the reference's encode_delta + decode_delta step for step on bytes "
+                      f"(oracle ref_encode_bytes / ref_decode_bytes), best of {reps}; "
+                      f"cpu: {model}"}
 
 
 def _cpu_model():

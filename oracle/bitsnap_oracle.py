@@ -82,6 +82,38 @@ def delta_decode(base: np.ndarray, mask: np.ndarray, payload: np.ndarray,
     return out
 
 
+def ref_encode_bytes(base: bytes, cur: bytes):
+    """bitmask.py:94-111 step for step on the TensorBlob byte strings the
+    reference works on (frombuffer views, count_nonzero, packbits, the
+    boolean gather, both tobytes copies and the record's length checks,
+    :44-54): the reference CPU cost of one encode, for the bench's CPU arm.
+    Returns (mask bytes, payload bytes, n_c)."""
+    b = np.frombuffer(base, dtype="<u2")
+    t = np.frombuffer(cur, dtype="<u2")
+    changed = b != t
+    n = int(changed.size)
+    n_c = int(np.count_nonzero(changed))
+    mask = np.packbits(changed, bitorder="little").tobytes()
+    payload = t[changed].tobytes()
+    if len(mask) != (n + 7) // 8 or len(payload) != 2 * n_c:
+        raise OracleDeltaError("record lengths")
+    return mask, payload, n_c
+
+
+def ref_decode_bytes(base: bytes, mask: bytes, payload: bytes, n: int, n_c: int) -> bytes:
+    """bitmask.py:114-140 step for step on bytes (unpackbits, padding check,
+    bool cast, popcount check, copy, scatter, the output tobytes copy)."""
+    bits = np.unpackbits(np.frombuffer(mask, dtype=np.uint8), bitorder="little")
+    if np.any(bits[n:]):
+        raise OracleDeltaError("nonzero padding bits in mask")
+    changed = bits[:n].astype(bool)
+    if int(np.count_nonzero(changed)) != n_c:
+        raise OracleDeltaError("mask popcount mismatch")
+    out = np.frombuffer(base, dtype="<u2").copy()
+    out[changed] = np.frombuffer(payload, dtype="<u2")
+    return out.tobytes()
+
+
 def delta_size(n: int, n_c: int) -> int:
     """bitmask.py:181-191 — serialized BSDL size for an empty name, rank 1."""
     if not 0 <= n_c <= n:

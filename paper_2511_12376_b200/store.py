@@ -404,7 +404,8 @@ class CheckpointEncoder:
         for p in plan["steps"]:
             if p[0] == "raw":
                 continue
-            with torch.cuda.stream(self._side[launched % len(self._side)]):
+            with torch.cuda.stream(self._side[launched % len(self._side)]), \
+                    rt.nvtx(f"{p[0]} {p[2].name}"):
                 di = self._launch_step(p, st, di, deltas, quants, mask_a, pay_a, lab_a, code_a,
                                        tab_a)
             launched += 1
@@ -575,8 +576,9 @@ class CheckpointEncoder:
         # arenas in memory)
         small = total <= GRAPH_MAX_ARENA
         with torch.cuda.device(self.dev):
-            for g in groups:
-                recs, md = self.encode_records(g, prev_map, kind, allow_graph=small)
+            for gi, g in enumerate(groups):
+                with rt.nvtx(f"save group {gi}"):
+                    recs, md = self.encode_records(g, prev_map, kind, allow_graph=small)
                 model_dev.update(md)
                 offs = [offsets[-1]]
                 for r in recs:
@@ -962,7 +964,8 @@ def decode_chain(chain, device: torch.device | None = None, to_host: bool = True
                 if manifest.kind == KIND_BASE:
                     model_order = [e.name for e in manifest.tensors if e.group == GROUP_MODEL]
                 plan.check_deltas(model, meta)
-                opt = plan.launch(dev, dblob, model, meta, checks, keep)
+                with rt.nvtx(f"restore link {ci} (iteration {manifest.iteration})"):
+                    opt = plan.launch(dev, dblob, model, meta, checks, keep)
                 if final:
                     final_opt = opt
                 ready.finish()

@@ -38,6 +38,21 @@ def test_bitmask_oracle_matches_reference_bytes(bitmask_golden, golden_index):
             8 * (len(case["shape"]) - 1) == len(want)
 
 
+def test_bitmask_byte_level_port_matches_reference(bitmask_golden, golden_index):
+    """The bench's CPU arm (oracle.ref_encode_bytes / ref_decode_bytes, the
+    reference's byte-level sequence) gives the reference's records."""
+    for case in golden_index["bitmask"]:
+        i = case["i"]
+        base, cur = bitmask_golden[f"c{i}_base"], bitmask_golden[f"c{i}_cur"]
+        bb = base.astype("<u2").tobytes()
+        cb = cur.astype("<u2").tobytes()
+        mask, payload, n_c = O.ref_encode_bytes(bb, cb)
+        got = O.delta_record(case["name"], case["shape"], base.size, n_c,
+                             np.frombuffer(mask, np.uint8), np.frombuffer(payload, "<u2"))
+        assert got == bitmask_golden[f"c{i}_bsdl"].tobytes(), case["name"]
+        assert O.ref_decode_bytes(bb, mask, payload, base.size, n_c) == cb
+
+
 def test_bitmask_kat_0x42(bitmask_golden, golden_index):
     case = next(c for c in golden_index["bitmask"] if c["name"] == "kat_0x42")
     blob = bitmask_golden[f"c{case['i']}_bsdl"].tobytes()
