@@ -1,22 +1,23 @@
 #!/bin/bash
-# Full GPU check: build, all GPU tests (+ the four-pass quantizer variant),
-# smoke, bench (b200 + reference arm), ncu launch list of the bench and a
-# full capture of the C1 and C2 top kernels.
+# Full GPU check: build, all GPU tests, smoke, bench (b200 + reference arm),
+# ncu launch list of the bench's kernels and a full capture of the C1 and C2
+# top kernels.  Outputs under gpurun_out/ with the given tag.
 tag=${1:-r}
 cd "${GRAFT_REPO_ROOT:-.}"; mkdir -p gpurun_out
 python -m paper_2511_12376_b200._build > gpurun_out/build_$tag.log 2>&1
 timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu_$tag.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu_$tag.log
-BSNP_WINDOW=0 timeout 900 python -m pytest tests/test_quantizer_gpu.py -q > gpurun_out/pytest_minmax_$tag.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_minmax_$tag.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$tag.log 2>&1; echo "rc=$?" >> gpurun_out/smoke_$tag.log
-timeout 900 python bench.py > gpurun_out/bench_$tag.json 2> gpurun_out/bench_$tag.err
+s=$(date +%s.%N)
+timeout 1200 python bench.py > gpurun_out/bench_$tag.json 2> gpurun_out/bench_$tag.err
+echo "bench wall $(echo "$(date +%s.%N) - $s" | bc) s rc=$?" >> gpurun_out/bench_$tag.err
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_$tag.json 2> gpurun_out/bench_ref_$tag.err
 if [ "${NCU:-1}" = 1 ]; then
-CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-c0"
+CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-c0 --no-ckpt --no-sweep"
 timeout 300 $CMD > gpurun_out/plain_$tag.log 2>&1 && \
-  timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+  timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file gpurun_out/launches_$tag.csv $CMD > gpurun_out/ncu_launch_$tag.log 2>&1 && \
-  timeout 1200 ncu --set full --clock-control none --import-source on \
-    -k "regex:delta_(encode_ws|decode_tma|offsets)" -c 3 -f -o gpurun_out/prof_$tag $CMD \
+  timeout 1500 ncu --set full --clock-control none --import-source on \
+    -k "regex:delta_(encode_ws|decode_tma|offsets)|fit_sum|fit_label|quantize_codes|dequantize_kernel" -c 8 -f -o gpurun_out/prof_$tag $CMD \
     > gpurun_out/ncu_full_$tag.log 2>&1
 fi
 echo done
