@@ -210,7 +210,7 @@ __device__ __forceinline__ uint32_t tile_local_scan(const uint32_t (&cnt)[kVec],
 // mbarriers: full[s] (TMA bytes), rec_full[r]/rec_empty[r] (workers <->
 // look-back warps), staged[r] (8 worker warps -> look-back warp).
 #ifndef BSNP_LB_WIDTH
-#define BSNP_LB_WIDTH 4  // look-back predecessors per lane per round trip
+#define BSNP_LB_WIDTH 2  // look-back predecessors per lane per round trip
 #endif
 #ifndef BSNP_KLB
 #define BSNP_KLB 2
@@ -225,7 +225,7 @@ constexpr int kEncStagesWS = 2;
 // still fit an SM; a tile too dense for it (> ~56 % changed) is staged in its
 // global scratch slot instead
 #ifndef BSNP_ARENA
-#define BSNP_ARENA 10240
+#define BSNP_ARENA 8192
 #endif
 constexpr uint32_t kArena = BSNP_ARENA;
 static_assert(kArena % 16 == 0, "arena granules");
