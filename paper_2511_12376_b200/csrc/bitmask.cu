@@ -576,15 +576,17 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
   for (int q0 = 0; q0 < kPerWarp; q0 += kOffBatch) {
     uint4 a[kOffBatch], b[kOffBatch];
-    bool full[kOffBatch];
+    uint32_t full = 0;  // bit q: tile q of the batch is loaded whole
 #pragma unroll
     for (int q = 0; q < kOffBatch; ++q) {
       const uint64_t t = chunk * kChunkTiles + warp * kPerWarp + q0 + q;
       const uint64_t b0 = t * kMaskBytes + (uint64_t)lane * 32;
-      full[q] = t < ntiles && vec && b0 + 32 < nbytes;  // the last byte goes the slow way
-      if (full[q]) {
+      if (t < ntiles && vec && b0 + 32 < nbytes) {  // the last byte goes the slow way
+        full |= 1u << q;
         a[q] = ld_stream_v4(mask + b0);
         b[q] = ld_stream_v4(mask + b0 + 16);
+      } else {
+        a[q] = b[q] = make_uint4(0, 0, 0, 0);
       }
     }
 #pragma unroll
@@ -592,7 +594,7 @@ __global__ void __launch_bounds__(kThreads)
       const int lt = warp * kPerWarp + q0 + q;
       const uint64_t t = chunk * kChunkTiles + lt;
       uint32_t c = 0;
-      if (full[q]) {
+      if ((full >> q) & 1u) {
         c = __popc(a[q].x) + __popc(a[q].y) + __popc(a[q].z) + __popc(a[q].w) +
             __popc(b[q].x) + __popc(b[q].y) + __popc(b[q].z) + __popc(b[q].w);
       } else if (t < ntiles) {
