@@ -908,7 +908,7 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
-    if world > 1:
+    if world > 1 or os.environ.get("BSNP_FORCE_PG"):
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
@@ -919,8 +919,8 @@ def main():
     try:
         run_b200(args, rank, world, local_rank)
     finally:
-        if world > 1:
-            import torch.distributed as dist
+        import torch.distributed as dist
+        if dist.is_initialized():
             dist.destroy_process_group()
 
 

@@ -73,7 +73,8 @@ def exchange_sizes(rows, world: int, max_rows: int | None = None, group=None,
     """All-gather this rank's (global_id, codec, count, bytes) rows.
 
     Returns an int64 tensor [world * max_rows, 4] on `device` (rows padded
-    with global_id = -1).  With world == 1 no collective is issued.
+    with global_id = -1).  Without a process group (a single-process save)
+    no collective is issued; with one, the all-gather runs at any world size.
     """
     import torch.distributed as dist
     max_rows = max(len(rows), 1) if max_rows is None else max(max_rows, 1)
@@ -88,7 +89,7 @@ def exchange_sizes(rows, world: int, max_rows: int | None = None, group=None,
     if rows:
         local[:len(rows)] = torch.tensor(rows, dtype=torch.int64)
     local = local.to(device)
-    if world == 1:
+    if world == 1 and not dist.is_initialized():
         return local
     out = torch.empty((world * max_rows, ROW), dtype=torch.int64, device=device)
     dist.all_gather_into_tensor(out, local, group=group)
