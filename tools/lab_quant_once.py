@@ -1,5 +1,5 @@
 """Quantizer lab: ONE C2-shaped encode after a warm-up (for ncu launch lists
-and full captures of the encode kernels; dev tool)."""
+and full captures of the encode kernels; DEQ=1 adds one dequantize; dev tool)."""
 import os
 import sys
 
@@ -20,5 +20,9 @@ labels = torch.empty(Q.unit_label_bytes(n, block), dtype=torch.uint8, device=dev
 codes = torch.empty(n, dtype=torch.uint8, device=dev)
 for _ in range(int(os.environ.get("REPS", "2"))):
     Q.cluster_encode_async(x, 16, block, tables, labels, codes)
+if os.environ.get("DEQ") == "1":  # and one dequantize of the result
+    out = torch.empty_like(x)
+    status = torch.zeros(4, dtype=torch.int64, device=dev)
+    Q.cluster_dequantize_async(labels, codes, n, block, tables, out, status)
 torch.cuda.synchronize()
 print("ok")
