@@ -92,8 +92,8 @@ int bsnp_delta_encode(const uint16_t* base, const uint16_t* target, uint64_t n,
  *   out[i] = changed[i] ? payload[rank(i)] : base[i]
  * out may equal base (in-place chain replay, store.py:441-454): the mask is
  * validated by a separate pre-pass first so that base is left untouched when
- * BSNP_ERR_PADDING / BSNP_ERR_POPCOUNT is raised.  Out-of-place decode is a
- * single pass; its `out` is undefined when a flag is raised.
+ * BSNP_ERR_PADDING / BSNP_ERR_POPCOUNT is raised.  Out of place, the decode
+ * does not wait for the validation: `out` is undefined when a flag is raised.
  */
 int bsnp_delta_decode(const uint16_t* base, const uint8_t* mask, const uint16_t* payload,
                       uint64_t n, uint64_t n_c, uint16_t* out, bsnp_status* status,
