@@ -951,29 +951,32 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // persistent grid size for a dynamic-smem kernel (attribute + occupancy
-// query once per kernel and thread: they cost microseconds per call)
+// query once per kernel, device and thread: they cost microseconds per call;
+// the shared-memory attribute is per device)
 template <typename K>
 int persistent_grid(K kernel, size_t smem, uint64_t work_items, int threads = kThreads) {
   struct Entry {
     const void* fn;
     size_t smem;
     int threads;
+    int dev;
     int blocks;
   };
-  thread_local Entry cache[8];
+  thread_local Entry cache[16];
   thread_local int used = 0;
+  int dev = 0;
+  const int sms = device_sms(&dev);
   int blocks = 0;
   for (int i = 0; i < used; ++i)
-    if (cache[i].fn == (const void*)kernel && cache[i].smem == smem && cache[i].threads == threads)
+    if (cache[i].fn == (const void*)kernel && cache[i].smem == smem &&
+        cache[i].threads == threads && cache[i].dev == dev)
       blocks = cache[i].blocks;
   if (!blocks) {
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int per_sm = 0;
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
     blocks = sms * (per_sm < 1 ? 1 : per_sm);
-    if (used < 8) cache[used++] = Entry{(const void*)kernel, smem, threads, blocks};
+    if (used < 16) cache[used++] = Entry{(const void*)kernel, smem, threads, dev, blocks};
   }
   const uint64_t g = (uint64_t)blocks < work_items ? (uint64_t)blocks : work_items;
   return (int)(g ? g : 1);
@@ -1096,12 +1099,7 @@ extern "C" int bsnp_delta_decode(const uint16_t* base, const uint8_t* mask,
     const int grid = persistent_grid(k, smem, nt);
     k<<<grid, kThreads, smem, s>>>(base, mask, payload, n, n_c, out, offsets, ticket2, status);
   } else if (in_place) {
-    static int sms = 0;
-    if (!sms) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int sms = device_sms();
     // one warp per tile, a few tiles per warp
     const uint64_t warps = (nt + 3) / 4;
     const uint64_t want = (warps + kWarps - 1) / kWarps;

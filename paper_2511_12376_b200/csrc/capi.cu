@@ -136,13 +136,7 @@ __global__ void __launch_bounds__(256)
 extern "C" int bsnp_copy_sm(const void* src, void* dst, uint64_t n, void* stream) {
   if (n == 0) return BSNP_OK;
   if (!src || !dst) return BSNP_E_INVALID;
-  static int sms = 0;  // one CTA per SM at most: small blocks, latency-bound
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms < 1) sms = 1;
-  }
+  const int sms = bsnp::device_sms();  // one CTA per SM at most: small blocks, latency-bound
   uint64_t grid = (n / 16 + 255) / 256;
   if (grid < 1) grid = 1;
   if (grid > (uint64_t)sms) grid = (uint64_t)sms;
