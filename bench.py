@@ -34,6 +34,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "bitmask delta encode+decode throughput (C1: 2^30 bf16, p changed)"
 FALLBACK_HBM_GBS = 6650.0
+NOMINAL_HBM_GBS = 8000.0   # the north star's nominal per-GPU HBM peak (reported beside "frac")
 
 
 def parse_args():
@@ -453,6 +454,7 @@ def run_b200(args, rank: int, world: int, local_rank: int):
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
                      "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": round(achieved / hbm, 4),
+                     "frac_of_nominal_8000": round(achieved / NOMINAL_HBM_GBS, 4),
                      "algorithmic_bytes": dom_bytes,
                      "traffic": traffic["bytes"] if traffic else None,
                      "traffic_detail": traffic},
@@ -599,11 +601,12 @@ def run_c1_sweep(args, dev, world, reps: int = 3):
 def run_c2_modes(args, dev, world, reps: int = 3):
     """BASELINE configs[2] in every form the bench quotes: Adam-m and Adam-v
     (v = |N(0,1e-3)|^2, one-sided, heavy-tailed), per 2^20 block and per
-    tensor (the store's layout), m = 16; encode and dequantize."""
+    tensor (the store's layout), m = 16; and the m sweep of SURVEY §8(d)
+    (m = 2 / 4 / 8, Adam-m per block); encode and dequantize."""
     import torch
     from paper_2511_12376_b200 import quantizer as Q
     from paper_2511_12376_b200 import _runtime as rt
-    n, m = 1 << args.c2_log2n, 16
+    n = 1 << args.c2_log2n
     hbm, kind = peaks()
     algo = 4 * n + n + (n + 1) // 2
     out = {}
@@ -612,7 +615,10 @@ def run_c2_modes(args, dev, world, reps: int = 3):
         x = torch.randn(n, device=dev, generator=g) * 1e-3
         if dist == "adam_v":
             x.mul_(x)
-        for block in (args.c2_block, 0):
+        runs = [(args.c2_block, 16), (0, 16)]
+        if dist == "adam_m":
+            runs += [(args.c2_block, mm) for mm in (2, 4, 8)]
+        for block, m in runs:
             tables = Q.new_tables(n, block, dev)
             labels = torch.empty(Q.unit_label_bytes(n, block), dtype=torch.uint8, device=dev)
             codes = torch.empty(n, dtype=torch.uint8, device=dev)
@@ -634,7 +640,8 @@ def run_c2_modes(args, dev, world, reps: int = 3):
             assert flags == 0 and maxlab < m
             units = Q.num_units(n, block)
             enc_bytes = Q.serialized_quant_size("t", 1, block or n, m) * units
-            out[f"{dist},block={block or 'tensor'}"] = {
+            key = f"{dist},block={block or 'tensor'}" + ("" if m == 16 else f",m={m}")
+            out[key] = {
                 "encode_ms": round(te, 4), "decode_ms": round(td, 4),
                 "encode_gbs": round(algo / (te * 1e-3) / 1e9, 1),
                 "decode_gbs": round(algo / (td * 1e-3) / 1e9, 1),
@@ -644,7 +651,8 @@ def run_c2_modes(args, dev, world, reps: int = 3):
                 "max_abs_err": float((res - x).abs().max())}
             del tables, labels, codes, res
         del x
-    return {"workload": f"C2 modes: 2^{args.c2_log2n} fp32, m = 16", "algorithmic_bytes": algo,
+    return {"workload": f"C2 modes: 2^{args.c2_log2n} fp32, m = 16 (and m = 2 / 4 / 8 for "
+                        "Adam-m per block)", "algorithmic_bytes": algo,
             "peak": hbm, "peak_kind": kind, "points": out}
 
 
@@ -842,12 +850,14 @@ def run_c2(args, dev, world):
             "roofline_encode": {"bound": "hbm", "achieved": round(enc_gbs / world, 1),
                                 "peak": hbm, "peak_kind": kind, "unit": "GB/s",
                                 "frac": round(enc_gbs / world / hbm, 4),
+                                "frac_of_nominal_8000": round(enc_gbs / world / NOMINAL_HBM_GBS, 4),
                                 "algorithmic_bytes": algo,
                                 "traffic": traffic["bytes"] if traffic else None,
                                 "traffic_detail": traffic},
             "roofline_decode": {"bound": "hbm", "achieved": round(dec_gbs / world, 1),
                                 "peak": hbm, "peak_kind": kind, "unit": "GB/s",
                                 "frac": round(dec_gbs / world / hbm, 4),
+                                "frac_of_nominal_8000": round(dec_gbs / world / NOMINAL_HBM_GBS, 4),
                                 "algorithmic_bytes": algo,
                                 "traffic": (ncu_traffic().get("cluster_dequantize") or {})
                                 .get("bytes"),
