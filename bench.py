@@ -371,25 +371,31 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     st = rt.new_status(dev, 2)
     stream = torch.cuda.current_stream(dev)
 
+    # the step never waits for the host: the decode reads n_c from the
+    # encode's status word on the device, and the size row of the
+    # multi-GPU exchange is built there too
+    row = torch.tensor([[0, 1, 0, (n + 7) // 8]], dtype=torch.int64, device=dev)
+
     def step(timing=None):
         if timing:
             timing[0].record(stream)
         B.encode_delta_async(base, cur, mask, payload, st[0])
         if timing:
             timing[1].record(stream)
-        (n_c, flags), = rt.read_status(st[0:1])
         if world > 1:
-            planner.exchange_sizes([(0, 1, n_c, (n + 7) // 8 + 2 * n_c)], world)
+            row[0, 2:3].copy_(st[0, 0:1])
+            row[0, 3:4].copy_(st[0, 0:1] * 2 + (n + 7) // 8)
+            planner.exchange_sizes(row, world)
         if timing:
             timing[2].record(stream)
-        B.decode_delta_async(base, mask, payload[:n_c], n_c, out, st[1])
+        B.decode_delta_async_dn(base, mask, payload, st[0], out, st[1])
         if timing:
             timing[3].record(stream)
-        return n_c, flags
 
     for _ in range(args.warmup):
-        n_c, flags = step()
-    assert n_c == k and flags == 0, (n_c, k, flags)
+        step()
+    (n_c, flags), (pc, dflags) = rt.read_status(st)
+    assert n_c == k and flags == 0 and pc == k and dflags == 0, (n_c, k, flags, pc, dflags)
     torch.cuda.synchronize(dev)
     # correctness of the timed configuration: decode(encode(cur)) == cur
     assert torch.equal(out, cur)
@@ -407,6 +413,8 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     t_end.record(stream)
     torch.cuda.synchronize(dev)
     clk = clocks.stop()
+    (n_c, flags), (pc, dflags) = rt.read_status(st)
+    assert n_c == k and flags == 0 and pc == k and dflags == 0, (n_c, k, flags, pc, dflags)
     ms = t_start.elapsed_time(t_end) / args.steps
     enc_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
     dec_ms = sum(e[2].elapsed_time(e[3]) for e in evs) / args.steps

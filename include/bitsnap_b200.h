@@ -99,6 +99,17 @@ int bsnp_delta_decode(const uint16_t* base, const uint8_t* mask, const uint16_t*
                       uint64_t n, uint64_t n_c, uint16_t* out, bsnp_status* status,
                       void* ws, size_t ws_bytes, void* stream);
 
+/*
+ * bsnp_delta_decode out of place with n_c read ON THE DEVICE from n_c_dev
+ * (e.g. &encode_status->count): an encode and the decode of its record run
+ * back to back with no host round trip.  payload holds the record's n_c
+ * elements; base, out and mask 16-byte aligned; out != base.  Same flags
+ * and status->count as bsnp_delta_decode.
+ */
+int bsnp_delta_decode_dn(const uint16_t* base, const uint8_t* mask, const uint16_t* payload,
+                         uint64_t n, const uint64_t* n_c_dev, uint16_t* out,
+                         bsnp_status* status, void* ws, size_t ws_bytes, void* stream);
+
 /* ------------------------------------------------------------------------
  * Cluster quantizer (reference quantizer.py:100-204)
  *

@@ -30,6 +30,7 @@ SIGNATURES = {
     "bsnp_delta_decode_ws_bytes": (_sz, [_u64]),
     "bsnp_delta_encode": (_i32, [_vp, _vp, _u64, _vp, _vp, _u64, _vp, _vp, _sz, _vp]),
     "bsnp_delta_decode": (_i32, [_vp, _vp, _vp, _u64, _u64, _vp, _vp, _vp, _sz, _vp]),
+    "bsnp_delta_decode_dn": (_i32, [_vp, _vp, _vp, _u64, _vp, _vp, _vp, _vp, _sz, _vp]),
     "bsnp_cluster_ws_bytes": (_sz, [_u64, _u64]),
     "bsnp_cluster_fit": (_i32, [_vp, _u64, _u64, _i32, _vp, _vp, _sz, _vp]),
     "bsnp_cluster_quantize": (_i32, [_vp, _u64, _u64, _vp, _vp, _vp, _vp, _sz, _vp]),

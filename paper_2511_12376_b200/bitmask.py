@@ -140,6 +140,24 @@ def decode_delta_async(base: torch.Tensor, mask: torch.Tensor, payload: torch.Te
         rt.stream_ptr(dev)), "bsnp_delta_decode")
 
 
+def decode_delta_async_dn(base: torch.Tensor, mask: torch.Tensor, payload: torch.Tensor,
+                          n_c_status: torch.Tensor, out: torch.Tensor,
+                          status: torch.Tensor) -> None:
+    """decode_delta_async out of place with n_c read on the device from
+    `n_c_status` (the encode's status block: its count word), so an encode
+    and the decode of its record queue back to back with no host round
+    trip (bsnp_delta_decode_dn).  payload: the encode's payload buffer."""
+    b = _as_i16(base)
+    o = out.reshape(-1).view(torch.int16)
+    n = b.numel()
+    dev = b.device
+    ws = rt.workspace(dev, rt.lib().bsnp_delta_decode_ws_bytes(n), "dec")
+    _lib.check(rt.lib().bsnp_delta_decode_dn(
+        b.data_ptr(), mask.data_ptr(), payload.data_ptr() if payload.numel() else None,
+        n, n_c_status.data_ptr(), o.data_ptr(), status.data_ptr(), ws.data_ptr(), ws.numel(),
+        rt.stream_ptr(dev)), "bsnp_delta_decode_dn")
+
+
 def _raise_decode_flags(flags: int, popcount: int, n_c: int) -> None:
     if flags & _lib.ERR_PADDING:
         raise DeltaError("nonzero padding bits in mask")

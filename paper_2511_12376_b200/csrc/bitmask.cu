@@ -561,7 +561,7 @@ __global__ void __launch_bounds__(kThreads)
     delta_offsets_kernel(const uint8_t* __restrict__ mask, uint64_t n, uint64_t n_c,
                          uint64_t* __restrict__ offsets, bsnp_status* __restrict__ st,
                          uint32_t* __restrict__ ticket, uint64_t* __restrict__ chunk_status,
-                         uint64_t nchunks) {
+                         uint64_t nchunks, const uint64_t* __restrict__ nc_dev = nullptr) {
   __shared__ uint32_t s_cnt[kChunkTiles];
   __shared__ uint32_t s_chunk;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -630,7 +630,7 @@ __global__ void __launch_bounds__(kThreads)
       const uint64_t pc = excl + total;
       offsets[ntiles] = pc;
       st->count = pc;
-      if (pc != n_c) atomicOr(&st->err_flags, BSNP_ERR_POPCOUNT);
+      if (pc != (nc_dev ? *nc_dev : n_c)) atomicOr(&st->err_flags, BSNP_ERR_POPCOUNT);
     }
   }
 }
@@ -638,10 +638,11 @@ __global__ void __launch_bounds__(kThreads)
 template <int kStages, bool kDense>
 __global__ void __launch_bounds__(kThreads)
     delta_decode_tma_kernel(const uint16_t* base, const uint8_t* __restrict__ mask,
-                            const uint16_t* __restrict__ payload, uint64_t n, uint64_t n_c,
+                            const uint16_t* __restrict__ payload, uint64_t n, uint64_t n_c_arg,
                             uint16_t* out, const uint64_t* __restrict__ offsets,
                             uint32_t* __restrict__ ticket,
-                            const bsnp_status* __restrict__ st) {
+                            const bsnp_status* __restrict__ st,
+                            const uint64_t* __restrict__ nc_dev = nullptr) {
   // in place (out == base, dense chain replay): every tile is read by TMA
   // into shared memory before its words are written, tiles are disjoint, and
   // a record the validation pass rejected leaves the base untouched
@@ -655,6 +656,9 @@ __global__ void __launch_bounds__(kThreads)
   __shared__ uint32_t s_off[kVec][kWarps];
 
   const int tid = threadIdx.x;
+  // n_c from the device (the encode's status word: no host round trip) or
+  // by value
+  const uint64_t n_c = nc_dev ? *nc_dev : n_c_arg;
   const uint64_t nfull = n / kTile;
   const uint64_t ntiles = (n + kTile - 1) / kTile;
   const uintptr_t p_lo = ((uintptr_t)payload + 15) & ~(uintptr_t)15;
@@ -1097,7 +1101,8 @@ extern "C" int bsnp_delta_decode(const uint16_t* base, const uint8_t* mask,
     const size_t smem = (size_t)kDecStages * kDecStage;
     auto k = delta_decode_tma_kernel<kDecStages, true>;
     const int grid = persistent_grid(k, smem, nt);
-    k<<<grid, kThreads, smem, s>>>(base, mask, payload, n, n_c, out, offsets, ticket2, status);
+    k<<<grid, kThreads, smem, s>>>(base, mask, payload, n, n_c, out, offsets, ticket2, status,
+                                   nullptr);
   } else if (in_place) {
     const int sms = device_sms();
     // one warp per tile, a few tiles per warp
@@ -1111,10 +1116,48 @@ extern "C" int bsnp_delta_decode(const uint16_t* base, const uint8_t* mask,
     auto k = n_c * 32 > n ? delta_decode_tma_kernel<kDecStages, true>
                           : delta_decode_tma_kernel<kDecStages, false>;
     const int grid = persistent_grid(k, smem, nt);
-    k<<<grid, kThreads, smem, s>>>(base, mask, payload, n, n_c, out, offsets, ticket2, nullptr);
+    k<<<grid, kThreads, smem, s>>>(base, mask, payload, n, n_c, out, offsets, ticket2, nullptr,
+                                   nullptr);
   } else {
     delta_apply_kernel<false><<<(unsigned)nt, kThreads, 0, s>>>(base, mask, payload, n, n_c,
                                                                  out, offsets, status);
   }
   return launch_status("delta_decode_kernel");
+}
+
+extern "C" int bsnp_delta_decode_dn(const uint16_t* base, const uint8_t* mask,
+                                    const uint16_t* payload, uint64_t n, const uint64_t* n_c_dev,
+                                    uint16_t* out, bsnp_status* status, void* ws,
+                                    size_t ws_bytes, void* stream) {
+  if (!status) return BSNP_E_INVALID;
+  if (n && (!base || !mask || !out || !ws || !n_c_dev)) return BSNP_E_INVALID;
+  if ((const void*)base == (const void*)out && n) return BSNP_E_INVALID;  // out of place only
+  if (((uintptr_t)base | (uintptr_t)out | (uintptr_t)payload) & 1) return BSNP_E_ALIGN;
+  const size_t need = bsnp_delta_decode_ws_bytes(n);
+  if (n && ws_bytes < need) return BSNP_E_WORKSPACE;
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = cuda_status("memset(status)", cudaMemsetAsync(status, 0, sizeof(bsnp_status), s));
+  if (rc || n == 0) return rc;
+  const uint64_t nt = num_tiles(n);
+  const uint64_t nchunks = (nt + kChunkTiles - 1) / kChunkTiles;
+  uint32_t* ticket = (uint32_t*)ws;
+  uint32_t* ticket2 = (uint32_t*)ws + 32;
+  uint64_t* cstat = (uint64_t*)((char*)ws + kWsHeader);
+  uint64_t* offsets = cstat + nchunks;
+  rc = cuda_status("memset(ws)", cudaMemsetAsync(ws, 0, kWsHeader + 8 * nchunks, s));
+  if (rc) return rc;
+  delta_offsets_kernel<<<(unsigned)nchunks, kThreads, 0, s>>>(mask, n, 0, offsets, status,
+                                                              ticket, cstat, nchunks, n_c_dev);
+  if ((rc = launch_status("delta_offsets_kernel"))) return rc;
+  const bool aligned = (((uintptr_t)base | (uintptr_t)out | (uintptr_t)mask) & 15) == 0;
+  if (aligned) {
+    // the sparse (bit-walk) expansion: n_c is not known on the host
+    const size_t smem = (size_t)kDecStages * kDecStage;
+    auto k = delta_decode_tma_kernel<kDecStages, false>;
+    const int grid = persistent_grid(k, smem, nt);
+    k<<<grid, kThreads, smem, s>>>(base, mask, payload, n, 0, out, offsets, ticket2, nullptr,
+                                   n_c_dev);
+    return launch_status("delta_decode_kernel");
+  }
+  return BSNP_E_ALIGN;
 }

@@ -70,25 +70,33 @@ def plan_shards(raw_bytes, world: int) -> ShardPlan:
 
 def exchange_sizes(rows, world: int, max_rows: int | None = None, group=None,
                    device: torch.device | None = None) -> torch.Tensor:
-    """All-gather this rank's (global_id, codec, count, bytes) rows.
+    """All-gather this rank's (global_id, codec, count, bytes) rows (a list,
+    or an int64 [k, 4] tensor, e.g. on the GPU).
 
     Returns an int64 tensor [world * max_rows, 4] on `device` (rows padded
     with global_id = -1).  Without a process group (a single-process save)
     no collective is issued; with one, the all-gather runs at any world size.
     """
     import torch.distributed as dist
-    max_rows = max(len(rows), 1) if max_rows is None else max(max_rows, 1)
-    if len(rows) > max_rows:
+    nrows = rows.shape[0] if isinstance(rows, torch.Tensor) else len(rows)
+    max_rows = max(nrows, 1) if max_rows is None else max(max_rows, 1)
+    if nrows > max_rows:
         raise ValueError("more rows than the plan allows")
     if device is None:
         if dist.is_initialized() and dist.get_backend(group) == "nccl":
             device = torch.device("cuda", torch.cuda.current_device())
         else:
             device = torch.device("cpu")
-    local = torch.full((max_rows, ROW), -1, dtype=torch.int64)
-    if rows:
-        local[:len(rows)] = torch.tensor(rows, dtype=torch.int64)
-    local = local.to(device)
+    if isinstance(rows, torch.Tensor):
+        # rows already on the device (e.g. counts the encoder left there):
+        # no host round trip before the all-gather
+        local = torch.full((max_rows, ROW), -1, dtype=torch.int64, device=device)
+        local[:nrows] = rows.to(device=device, dtype=torch.int64)
+    else:
+        local = torch.full((max_rows, ROW), -1, dtype=torch.int64)
+        if rows:
+            local[:nrows] = torch.tensor(rows, dtype=torch.int64)
+        local = local.to(device)
     if world == 1 and not dist.is_initialized():
         return local
     out = torch.empty((world * max_rows, ROW), dtype=torch.int64, device=device)

@@ -282,3 +282,35 @@ def test_in_place_apply_dense(dev, n, p):
     with pytest.raises(B.DeltaError, match="popcount"):
         B.decode_delta_device(bt, bad, d.payload, d.n_c, out=bt)
     assert np.array_equal(bt.cpu().numpy().view(np.uint16), base)
+
+
+@pytest.mark.parametrize("n,p", [(8192, 0.01), (65536 * 5 + 8, 0.001), ((1 << 20) + 16, 0.05),
+                                 ((1 << 22) + 8, 0.3)])
+def test_decode_with_device_count(dev, n, p):
+    """bsnp_delta_decode_dn: the decode reads n_c from the encode's status
+    word on the device (no host round trip between the two): the result is
+    the target, status->count the popcount, and a count that disagrees with
+    the mask raises the reference's popcount error."""
+    import torch
+    from paper_2511_12376_b200 import _runtime as rt
+    from paper_2511_12376_b200 import bitmask as B
+    rng = np.random.default_rng(n)
+    base = rng.integers(0, 1 << 16, n, dtype=np.uint16)
+    cur = base.copy()
+    idx = rng.choice(n, int(n * p), replace=False)
+    cur[idx] ^= rng.integers(1, 1 << 16, idx.size, dtype=np.uint16)
+    bt, ct = _dev_u16(base, dev), _dev_u16(cur, dev)
+    mask = torch.empty((n + 7) // 8, dtype=torch.uint8, device=dev)
+    pay = torch.empty(n, dtype=torch.int16, device=dev)
+    out = torch.empty_like(bt)
+    st = rt.new_status(dev, 2)
+    B.encode_delta_async(bt, ct, mask, pay, st[0])
+    B.decode_delta_async_dn(bt, mask, pay, st[0], out, st[1])
+    (n_c, f0), (pc, f1) = rt.read_status(st)
+    assert n_c == pc == idx.size and f0 == f1 == 0
+    assert np.array_equal(out.cpu().numpy().view(np.uint16), cur)
+    bad = torch.tensor([idx.size + 1, 0], dtype=torch.int64, device=dev)
+    B.decode_delta_async_dn(bt, mask, pay, bad, out, st[1])
+    (pc, f1), = rt.read_status(st[1:2])
+    with pytest.raises(B.DeltaError, match="popcount"):
+        B._raise_decode_flags(f1, pc, idx.size + 1)
