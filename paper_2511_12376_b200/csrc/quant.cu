@@ -1145,14 +1145,12 @@ int run_fit(const float* x, const QPlan& P, bsnp_cluster_table* tables, const QW
 }
 
 // Encode (labels != nullptr) or fit only: the threshold-window tiled path
-// (quant_window.cuh); BSNP_WINDOW=0 selects the original min/max + quantize
-// kernels.
+// (quant_window.cuh); BSNP_WINDOW=0 selects the four-pass kernels (mean
+// tree, variance tree, per-element min/max, quantize) — a second exact
+// implementation the tests compare with (read per call so a test can switch)
 bool window_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("BSNP_WINDOW");
-    return !(e && atoi(e) == 0);
-  }();
-  return on;
+  const char* e = getenv("BSNP_WINDOW");
+  return !(e && atoi(e) == 0);
 }
 
 // BSNP_VAR_EXACT=1: every unit takes numpy's variance tree (tests of the

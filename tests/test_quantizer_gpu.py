@@ -403,3 +403,24 @@ def test_precision_report_deterministic(dev):
     want = O.precision(x.cpu().numpy(), y.cpu().numpy())
     assert reps[0]["mse"] == pytest.approx(want["mse"], rel=1e-9)
     assert reps[0]["mre"] == pytest.approx(want["mre"], rel=1e-9)
+
+
+@pytest.mark.parametrize("n,block,dist,m", [
+    ((1 << 20) + 5, 0, "adam_m", 16), (100003, 8192, "adam_v", 7),
+    (3 * (1 << 16) + 1000, 1 << 16, "uniform", 2), (9 * 8192, 8192, "discrete", 16),
+    (5000, 0, "adam_v", 16)])
+def test_four_pass_path_matches_window_path(dev, monkeypatch, n, block, dist, m):
+    """BSNP_WINDOW=0 runs the four-pass kernels (numpy's mean tree, variance
+    tree, per-element min/max with fit labels, then quantize): a second exact
+    implementation of quantizer.py:100-189.  Both are bit-exact vs the
+    oracle and give identical bytes."""
+    from paper_2511_12376_b200 import quantizer as Q
+    rng = np.random.default_rng(n * 3 + m)
+    x = _dist(dist, n, rng).astype(np.float32)
+    xt = _f32(x, dev)
+    a = Q.cluster_encode_device(xt, m, block)
+    monkeypatch.setenv("BSNP_WINDOW", "0")
+    b = Q.cluster_encode_device(xt, m, block)
+    _check_units(x, m, block, b)
+    for f in ("tables", "labels", "codes"):
+        assert bytes(getattr(a, f).cpu().numpy()) == bytes(getattr(b, f).cpu().numpy()), f
