@@ -494,6 +494,17 @@ def run_b200(args, rank: int, world: int, local_rank: int):
             c0cpu = cpu_baseline_c0()
             c0cpu["value_1core"] = cpu_baseline_c0(cores=1, max_elems=3_000_000)["value"]
             line["cpu_baseline_c0"] = c0cpu
+            # C3 / C4 on the CPU by extrapolation from a timed
+            # sample — here the C0 whole-checkpoint rate (the same codec mix:
+            # bf16 deltas + quantized fp32 states) scaled by raw bytes
+            for key in ("c3_sharded", "c4_sharded"):
+                if key in line and c0cpu["value"] > 0:
+                    raw = line[key]["raw_bytes"]
+                    line[key]["cpu_extrapolated"] = {
+                        "save_delta_s": round(raw / (c0cpu["value"] * 1e9), 1),
+                        "cores": c0cpu["cores"], "kind": "port, extrapolated",
+                        "basis": "cpu_baseline_c0 rate (numpy oracle encode_checkpoint, "
+                                 "all host cores) x this checkpoint's raw bytes"}
     print(json.dumps(line), flush=True)
 
 
