@@ -103,7 +103,8 @@ def ncu_traffic():
 class Clocks:
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,"
+         "clocks.mem,temperature.gpu,temperature.memory")
 
     def __init__(self, index: int):
         self.index = index
@@ -145,8 +146,27 @@ class Clocks:
             for name, v in zip(names, r[5:9]):
                 if v.lower().startswith("active"):
                     reasons.add(name)
-        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": int(rows[0][2]),
-                "samples": len(rows), "reasons": sorted(reasons)}
+        out = {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": int(rows[0][2]),
+               "samples": len(rows), "reasons": sorted(reasons)}
+
+        def num(i):
+            vals = []
+            for r in rows:
+                try:
+                    vals.append(float(r[i]))
+                except (IndexError, ValueError):
+                    pass
+            return vals
+        mem, tg, tm, pw = num(9), num(10), num(11), num(3)
+        if mem:
+            out["mem_mhz"] = int(sorted(mem)[len(mem) // 2])
+        if tg:
+            out["gpu_temp_c_max"] = max(tg)
+        if tm:
+            out["hbm_temp_c_max"] = max(tm)
+        if pw:
+            out["power_w_max"] = max(pw)
+        return out
 
 
 # ---------------------------------------------------------------------------
@@ -629,6 +649,8 @@ def run_c2_modes(args, dev, world, reps: int = 3):
     hbm, kind = peaks()
     algo = 4 * n + n + (n + 1) // 2
     out = {}
+    clocks = Clocks(dev.index or 0)
+    clocks.start()
     for dist in ("adam_m", "adam_v"):
         g = torch.Generator(device=dev).manual_seed(args.seed + (7 if dist == "adam_m" else 8))
         x = torch.randn(n, device=dev, generator=g) * 1e-3
@@ -670,9 +692,10 @@ def run_c2_modes(args, dev, world, reps: int = 3):
                 "max_abs_err": float((res - x).abs().max())}
             del tables, labels, codes, res
         del x
+    clk = clocks.stop()
     return {"workload": f"C2 modes: 2^{args.c2_log2n} fp32, m = 16 (and m = 2 / 4 / 8 for "
                         "Adam-m per block)", "algorithmic_bytes": algo,
-            "peak": hbm, "peak_kind": kind, "points": out}
+            "peak": hbm, "peak_kind": kind, "points": out, "clocks": clk}
 
 
 def run_ckpt_sharded(config, dev, rank, world, reps: int = 2):
@@ -843,6 +866,8 @@ def run_c2(args, dev, world):
     if world > 1:
         dist.barrier()
     te = td = 0.0
+    clocks = Clocks(dev.index or 0)
+    clocks.start()
     for _ in range(args.steps):
         ev[0].record(stream)
         Q.cluster_encode_async(x, m, block, tables, labels, codes)
@@ -852,6 +877,7 @@ def run_c2(args, dev, world):
         torch.cuda.synchronize(dev)
         te += ev[0].elapsed_time(ev[1])
         td += ev[1].elapsed_time(ev[2])
+    clk = clocks.stop()
     te /= args.steps
     td /= args.steps
     if world > 1:
@@ -882,7 +908,7 @@ def run_c2(args, dev, world):
                                 .get("bytes"),
                                 "traffic_detail": ncu_traffic().get("cluster_dequantize")},
             "compression_ratio": round(4 * n / enc_bytes, 4),
-            "max_abs_err": err}
+            "max_abs_err": err, "clocks": clk}
 
 
 def run_e2e(args, base, cur, k, dev, world):
