@@ -219,7 +219,10 @@ constexpr int kLB = BSNP_KLB;  // look-back warps per CTA
 constexpr int kRing = 16;
 static_assert(kRing % kLB == 0, "ring slots map to look-back warps");
 constexpr int kEncThreads = kThreads + 32 * kLB;
-constexpr int kEncStagesWS = 2;
+#ifndef BSNP_ENC_STAGES
+#define BSNP_ENC_STAGES 2
+#endif
+constexpr int kEncStagesWS = BSNP_ENC_STAGES;  // TMA stages (base + cur tiles)
 // compacted payloads of the tiles in flight wait for their prefix in a
 // shared-memory arena (a byte ring, 16-byte granules) sized so three CTAs
 // still fit an SM; a tile too dense for it (> ~56 % changed) is staged in its
@@ -324,18 +327,11 @@ __global__ void __launch_bounds__(kEncThreads)
       const uint32_t b0 = in_arena ? abase % kArena : 0;
       // record source: byte ring of the arena, or the tile's global slot
       auto granule = [&](uint32_t o) {  // 16 bytes at source byte o (16-aligned)
-        if (in_arena) {
-          if (o >= kArena) o -= kArena;
-          return *reinterpret_cast<const uint4*>(arena + o);
-        }
+        if (in_arena) return *reinterpret_cast<const uint4*>(arena + o);
         return __ldcg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(src) + o));
       };
       auto elem = [&](uint32_t i) -> uint16_t {
-        if (in_arena) {
-          uint32_t o = b0 + 2 * i;
-          if (o >= kArena) o -= kArena;
-          return reinterpret_cast<const uint16_t*>(arena)[o >> 1];
-        }
+        if (in_arena) return reinterpret_cast<const uint16_t*>(arena)[(b0 >> 1) + i];
         return src[i];
       };
       if (!overflow) {
@@ -348,9 +344,7 @@ __global__ void __launch_bounds__(kEncThreads)
         if ((uint32_t)lane < h) dst[lane] = elem(lane);
         const uint32_t nv = (c - h) / 8;
         for (uint32_t v = lane; v < nv; v += 32) {
-          uint32_t o = b0 + 2 * h + 16 * v;  // first source byte
-          if (in_arena)
-            while (o >= kArena) o -= kArena;
+          const uint32_t o = b0 + 2 * h + 16 * v;  // first source byte
           const uint32_t g = o & ~15u;
           const uint4 lo = granule(g), hi = granule(g + 16);
           const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
@@ -465,8 +459,12 @@ __global__ void __launch_bounds__(kEncThreads)
     // a tile that does not fit NOW goes to its global slot (never wait: a
     // blocked CTA would hold back the aggregates other CTAs look back on)
     const uint32_t abytes = (2 * total + 15) & ~15u;
-    const bool in_arena = arena_head + abytes - s_snap[db] <= kArena;
-    const uint32_t abase = in_arena ? arena_head : kDenseTile;
+    // records never straddle the ring's end (the remainder is skipped), so
+    // neither the compaction nor the look-back warp's copy wraps per element
+    uint32_t start = arena_head;
+    if (start % kArena + abytes > kArena) start += kArena - start % kArena;
+    const bool in_arena = start + abytes - s_snap[db] <= kArena;
+    const uint32_t abase = in_arena ? start : kDenseTile;
     if (warp == 0 && lane == 0) {
       publish_aggregate(tile_status, tile, total);
       push_record(q, tile, total, abase);
@@ -479,7 +477,7 @@ __global__ void __launch_bounds__(kEncThreads)
       if (g * 8 < n) mask[g] = (uint8_t)bits[j];
     }
     if (in_arena) {
-      arena_head += abytes;
+      arena_head = start + abytes;
       uint16_t* a16 = reinterpret_cast<uint16_t*>(arena);
       const uint32_t b0 = abase % kArena;
       if (total >= kDenseCompact) {
@@ -493,8 +491,7 @@ __global__ void __launch_bounds__(kEncThreads)
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             if ((b >> k) & 1u) {
-              uint32_t o = o0 + 2 * __popc(b & ((1u << k) - 1u));
-              if (o >= kArena) o -= kArena;
+              const uint32_t o = o0 + 2 * __popc(b & ((1u << k) - 1u));
               a16[o >> 1] = (uint16_t)(w4[k >> 1] >> (16 * (k & 1)));
             }
           }
@@ -507,7 +504,7 @@ __global__ void __launch_bounds__(kEncThreads)
           while (b) {
             const uint32_t k = __ffs(b) - 1;
             b &= b - 1;
-            a16[(o >= kArena ? o - kArena : o) >> 1] = (uint16_t)u16_lane(cv[j], k);
+            a16[o >> 1] = (uint16_t)u16_lane(cv[j], k);
             o += 2;
           }
         }
@@ -1007,7 +1004,9 @@ static size_t enc_scratch_offset(uint64_t n) {
   return align_up(kWsHeader + 8 * (size_t)num_tiles(n), 256);
 }
 
-static size_t enc_smem() { return (size_t)kEncStagesWS * kEncStage + kArena; }
+// + 32 bytes: the look-back warp's funnel-shifted copy reads up to two
+// granules past a record that ends at the arena's end
+static size_t enc_smem() { return (size_t)kEncStagesWS * kEncStage + kArena + 32; }
 
 // global staging slots of tiles too dense for the arena: one per tile, or a
 // ring of kRing per CTA when that is fewer (large tensors: 2^30 elements
