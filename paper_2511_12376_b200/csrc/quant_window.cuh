@@ -488,17 +488,23 @@ __device__ __forceinline__ void codes_chunk(const float* __restrict__ x, const Q
   float* qs = cs.qs;
   const int tid = threadIdx.x;
   const bsnp_cluster_table& tb = tables[r.u];
+  bool finite_rc = true;
   if (tid < 16) {
     const float S_ = __ldcg(tb.scales + tid);
     float rc = 0.0f;
     if (S_ > 0.0f) {
       rc = __fdiv_rn(255.0f, S_);
-      if (!isfinite(rc)) rc = __int_as_float(0x7fffffff);
+      if (!isfinite(rc)) {
+        rc = __int_as_float(0x7fffffff);
+        finite_rc = false;
+      }
     }
     qp[tid] = make_float2(__ldcg(tb.offsets + tid), rc);
     qs[tid] = S_;
   }
-  __syncthreads();
+  // every 255/S finite (all but subnormal-width clusters): the fixed-point
+  // fast path below
+  const bool fast = __syncthreads_and(finite_rc) != 0;
   const float* src = x + r.ustart + r.c0;
   uint8_t* cdst = codes + r.ustart + r.c0;
   const uint8_t* lab = labels + (uint64_t)r.u * (P.block / 2) + r.c0 / 2;
@@ -506,7 +512,60 @@ __device__ __forceinline__ void codes_chunk(const float* __restrict__ x, const Q
   const bool vec = ((((uintptr_t)src) & 15) | (((uintptr_t)cdst) & 3) | (((uintptr_t)lab) & 1)) == 0;
   const uint32_t nv = vec ? size / 4 : 0;
   constexpr int kB = 4;  // vectors per thread in flight
-  for (uint32_t i0 = tid; i0 < nv; i0 += kB * kQThreads) {
+  if (fast) {
+    // T = RN(RN(v - b) * rc + 3071.5) lies within 1.53e-4 of
+    // 255 (v - b) / S + 3071.5 (relative error of d * rc <= 2^-23 + 2^-48 on
+    // |z| <= 257, plus half an ulp, 2^-13, of T in [2^11, 2^12)); once T is
+    // clamped to [3071 + 2^-12, 3327 - 2^-12], (bits(T) - bits(3071) >> 12)
+    // is the code ceil(255 x - 0.5) clipped to [0, 255] unless T is an
+    // integer (its 12 fraction bits are 0: within 1.53e-4 < 2^-12 of a code
+    // boundary), when the reference's float64 expression decides.  The
+    // reference's own float64 roundings are ~1e-13 from the exact value, far
+    // inside the 2^-12 - 1.53e-4 margin.  NaN T (a NaN element) clamps to
+    // code 0 as exact_code does.
+    constexpr float kK = 3071.5f, kLo = 3071.000244140625f, kHi = 3326.999755859375f;
+    constexpr uint32_t kBase = 0x453FF000u;  // bits(3071.0f)
+    for (uint32_t i0 = tid; i0 < nv; i0 += kB * kQThreads) {
+      float4 v4[kB];
+      uint32_t lw[kB];
+#pragma unroll
+      for (int b = 0; b < kB; ++b) {
+        const uint32_t i = i0 + b * kQThreads;
+        if (i < nv) {
+          v4[b] = ld_hint_f4(src + 4 * i, pol);
+          lw[b] = __ldcg(reinterpret_cast<const unsigned short*>(lab) + i);
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < kB; ++b) {
+        const uint32_t i = i0 + b * kQThreads;
+        if (i >= nv) break;
+        const float v[4] = {v4[b].x, v4[b].y, v4[b].z, v4[b].w};
+        uint32_t c[4], fmin = 0xfffu;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 bp = qp[(lw[b] >> (4 * q)) & 15u];
+          const float t = __fmaf_rn(__fsub_rn(v[q], bp.x), bp.y, kK);
+          const uint32_t u = __float_as_uint(fminf(fmaxf(t, kLo), kHi));
+          c[q] = (u - kBase) >> 12;
+          fmin = min(fmin, u & 0xfffu);
+        }
+        if (__builtin_expect(fmin == 0, 0)) {
+          // some T is an integer: those elements take the exact path
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t k = (lw[b] >> (4 * q)) & 15u;
+            const float t = __fmaf_rn(__fsub_rn(v[q], qp[k].x), qp[k].y, kK);
+            if ((__float_as_uint(fminf(fmaxf(t, kLo), kHi)) & 0xfffu) == 0)
+              c[q] = exact_code(v[q], qp[k].x, qs[k]);
+          }
+        }
+        *reinterpret_cast<uint32_t*>(cdst + 4 * i) =
+            __byte_perm(__byte_perm(c[0], c[1], 0x0040), __byte_perm(c[2], c[3], 0x0040), 0x5410);
+      }
+    }
+  }
+  for (uint32_t i0 = tid; !fast && i0 < nv; i0 += kB * kQThreads) {
     float4 v4[kB];
     uint32_t lw[kB];
 #pragma unroll
