@@ -1030,8 +1030,8 @@ __global__ void __launch_bounds__(kQThreads)
   }
 }
 
-#include "quant_stats.cuh"
 #include "quant_window.cuh"
+#include "quant_stats.cuh"
 
 // ---------------------------------------------------------------- host plan
 uint32_t tree_depth(uint64_t len) {
@@ -1173,19 +1173,20 @@ int run_window(const float* x, const QPlan& P, bsnp_cluster_table* tables, uint8
         P, w.partials, w.partials_q, w.partials2, w.partials2_q);
     if ((rc = launch_status("pre_combine2_kernel"))) return rc;
   }
+  // statistics + the bin grid of every unit the sigma interval decides; the
+  // listed units get numpy's variance tree and their grid afterwards
   fit_stats_kernel<<<P.nunits, kQThreads, 0, s>>>(x, P, w.partials, w.partials_q, w.partials2,
                                                    w.partials2_q, w.mu, w.fthr, tables, w.sd,
-                                                   w.list, var_exact_forced());
+                                                   w.list, var_exact_forced(), w.ug,
+                                                   w.need + P.nunits);
   if ((rc = launch_status("fit_stats_kernel"))) return rc;
-  fit_var_fallback_kernel<<<(unsigned)std::min<uint64_t>(tiles, 2048), kQThreads, 0, s>>>(
-      x, P, w.mu, w.list, w.partials);
+  fit_var_fallback_kernel<<<(unsigned)std::min<uint64_t>(tiles, 2 * (uint64_t)device_sms()),
+                            kQThreads, 0, s>>>(x, P, w.mu, w.list, w.partials);
   if ((rc = launch_status("fit_var_fallback_kernel"))) return rc;
   fit_var_combine_kernel<<<std::min(P.nunits, 256u), kQThreads, 0, s>>>(P, w.partials, w.list,
                                                                         w.mu, w.fthr, tables,
-                                                                        w.sd);
+                                                                        w.sd, w.ug);
   if ((rc = launch_status("fit_var_combine_kernel"))) return rc;
-  fit_grid_kernel<<<P.nunits, kQThreads, 0, s>>>(P, w.mu, w.sd, w.ug, w.need + P.nunits);
-  if ((rc = launch_status("fit_grid_kernel"))) return rc;
   const unsigned chunks = (unsigned)((uint64_t)(P.nunits - 1) * P.C_full + P.C_last);
   fit_label_kernel<<<chunks, kQThreads, 0, s>>>(x, P, w.ug, labels);
   if ((rc = launch_status("fit_label_kernel"))) return rc;

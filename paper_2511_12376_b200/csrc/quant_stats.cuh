@@ -238,9 +238,15 @@ __global__ void __launch_bounds__(kQThreads)
                      const double* __restrict__ partials_q, const double* __restrict__ partials2,
                      const double* __restrict__ partials2_q, double* __restrict__ mu,
                      float* __restrict__ fthr, bsnp_cluster_table* __restrict__ tables,
-                     double* __restrict__ sdv, uint32_t* __restrict__ list, int force_exact) {
+                     double* __restrict__ sdv, uint32_t* __restrict__ list, int force_exact,
+                     UGrid* __restrict__ ug, uint32_t* __restrict__ any_need) {
   __shared__ double sv[kQThreads];
+  __shared__ GridSmem g;
+  __shared__ double s_mean, s_sd;
+  __shared__ uint32_t s_ok;
   const uint32_t u = blockIdx.x;
+  // the "some unit needs the exact min/max round" word, set by fit_decide
+  if (u == 0 && threadIdx.x == 0) *any_need = 0;
   uint32_t T;
   uint64_t len;
   unit_shape(P, u, T, len);
@@ -249,21 +255,30 @@ __global__ void __launch_bounds__(kQThreads)
   const double S = combine_perfect((sh ? partials2 : partials) + first, T >> sh, sv);
   __syncthreads();
   const double D2 = combine_perfect((sh ? partials2_q : partials_q) + first, T >> sh, sv);
-  if (threadIdx.x != 0) return;
-  const double ld = (double)len;
-  const double mean = __ddiv_rn(__dadd_rn(0.0, S), ld);  // np.mean
-  mu[u] = mean;
-  double sd;
-  const double c = (double)x[(uint64_t)u * P.block];
-  if (!force_exact && sigma_from_d2(S, D2, c, ld, mean, (int)P.m, sd)) {
-    write_header(P, u, mean, sd, fthr, tables, sdv);
-  } else if (!isfinite(mean)) {
-    // NaN / Inf in the unit: the host raises; any sd will do
-    write_header(P, u, mean, mean, fthr, tables, sdv);
-  } else {
-    const uint32_t i = atomicAdd(list, 1u);
-    list[1 + i] = u;
+  if (threadIdx.x == 0) {
+    const double ld = (double)len;
+    const double mean = __ddiv_rn(__dadd_rn(0.0, S), ld);  // np.mean
+    mu[u] = mean;
+    double sd;
+    const double c = (double)x[(uint64_t)u * P.block];
+    uint32_t ok = 1;
+    if (!force_exact && sigma_from_d2(S, D2, c, ld, mean, (int)P.m, sd)) {
+      write_header(P, u, mean, sd, fthr, tables, sdv);
+    } else if (!isfinite(mean)) {
+      // NaN / Inf in the unit: the host raises; any sd will do
+      sd = mean;
+      write_header(P, u, mean, sd, fthr, tables, sdv);
+    } else {
+      const uint32_t i = atomicAdd(list, 1u);
+      list[1 + i] = u;
+      ok = 0;
+    }
+    s_mean = mean;
+    s_sd = sd;
+    s_ok = ok;
   }
+  __syncthreads();
+  if (s_ok) grid_unit(P, u, s_mean, s_sd, ug, g);
 }
 
 // numpy's variance tree for the listed units only (grid-stride over their
@@ -291,8 +306,10 @@ __global__ void __launch_bounds__(kQThreads)
     fit_var_combine_kernel(QPlan P, const double* __restrict__ partials,
                            const uint32_t* __restrict__ list, const double* __restrict__ mu,
                            float* __restrict__ fthr, bsnp_cluster_table* __restrict__ tables,
-                           double* __restrict__ sdv) {
+                           double* __restrict__ sdv, UGrid* __restrict__ ug) {
   __shared__ double sv[kQThreads];
+  __shared__ GridSmem g;
+  __shared__ double s_sd;
   const uint32_t cnt = __ldcg(list);
   for (uint32_t i = blockIdx.x; i < cnt; i += gridDim.x) {
     const uint32_t u = __ldcg(list + 1 + i);
@@ -304,6 +321,9 @@ __global__ void __launch_bounds__(kQThreads)
     if (threadIdx.x == 0) {
       const double sd = __dsqrt_rn(__ddiv_rn(__dadd_rn(0.0, S), (double)len));  // np.std
       write_header(P, u, mu[u], sd, fthr, tables, sdv);
+      s_sd = sd;
     }
+    __syncthreads();
+    grid_unit(P, u, mu[u], s_sd, ug, g);  // the unit's bin grid (fit_stats skipped it)
   }
 }

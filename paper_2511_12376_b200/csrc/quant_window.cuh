@@ -4,8 +4,10 @@
 // The fit's per-cluster min/max pass and the quantize pass of the tiled
 // kernels are replaced by:
 //
-//   fit_grid_kernel   (per unit)  bin grid over mu +- 2 sd, a 1024-bin label
-//                                 LUT and the threshold window delta
+//   grid_unit         (per unit)  bin grid over mu +- 2 sd, a 16384-bin label
+//                                 LUT and the threshold window delta (built
+//                                 by fit_stats_kernel, quant_stats.cuh, or
+//                                 after the exact variance tree)
 //   fit_label_kernel  (per tile)  quantize labels (written out: they are the
 //                                 final label stream) + unit extremes +
 //                                 candidates within delta of the fit
@@ -173,16 +175,6 @@ __device__ __forceinline__ void grid_unit(const QPlan& P, uint32_t u, double m0,
   __syncthreads();
   for (int i = tid; i < kWBins / 16; i += kQThreads)
     reinterpret_cast<uint4*>(G.lut)[i] = reinterpret_cast<const uint4*>(lut)[i];
-}
-
-// any_need (optional): the "some unit needs the exact round" word, cleared
-// here for fit_decide_kernel to set
-__global__ void __launch_bounds__(kQThreads)
-    fit_grid_kernel(QPlan P, const double* __restrict__ mu, const double* __restrict__ sdv,
-                    UGrid* __restrict__ ug, uint32_t* __restrict__ any_need = nullptr) {
-  __shared__ GridSmem g;
-  if (any_need && blockIdx.x == 0 && threadIdx.x == 0) *any_need = 0;
-  grid_unit(P, blockIdx.x, mu[blockIdx.x], sdv[blockIdx.x], ug, g);
 }
 
 // elementwise passes run over kDqChunk-element chunks of each unit (the

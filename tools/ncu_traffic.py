@@ -15,7 +15,7 @@ GROUPS = {
     "delta_encode": ["delta_encode_ws_kernel"],
     "delta_decode": ["delta_offsets_kernel", "delta_decode_tma_kernel<2, 0>"],
     "cluster_encode": ["fit_sum_kernel", "fit_stats_kernel", "fit_var_fallback_kernel",
-                       "fit_var_combine_kernel", "fit_grid_kernel", "fit_label_kernel",
+                       "fit_var_combine_kernel", "fit_label_kernel",
                        "fit_decide_kernel", "fit_minmax_kernel", "fit_finalize_kernel",
                        "quantize_codes_kernel"],
     "cluster_dequantize": ["dequantize_kernel"],
