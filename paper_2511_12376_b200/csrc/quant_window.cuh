@@ -26,9 +26,11 @@
 // lo <= F_k exists, every element in (lo, F_k] has label k and lies within
 // delta, so it is a candidate too: lo is pred(F_k).  Likewise for succ
 // (elements in (F_k, hi) have label k+1, or equal B32_k > F_k with label k).
-// delta = 80 sd / n: for dense data pred/succ are ~sd/(n pdf) away (<= 8.3
-// sd / n for every threshold of m <= 16), so a missing side (probability
-// <= e^-9.6 per threshold side) only costs the exact round of that unit.
+// delta = 160 sd / n: for dense data pred/succ are ~sd/(n pdf) away (<= 8.3
+// sd / n for every threshold of m <= 16 on Gaussian data), so a missing side
+// only costs the exact round of that unit; one-sided heavy-tailed data
+// (Adam-v) has thresholds in thinner tails, where 160 instead of 80 sd / n
+// halves the units sent to the exact round (C2 Adam-v: 2.57 -> 2.48 ms).
 // LUT byte: bits 0-3 L = #quantize boundaries in lower bins; bit 7: boundary L
 // lies in this bin (label = L + (v > B32[L])); bit 6: kLutN below.
 constexpr uint32_t kLutB = 0x80u;
@@ -58,7 +60,10 @@ __device__ __forceinline__ uint32_t ceil_u8(float t) {
   return r;
 }
 
-constexpr uint32_t kWDeltaNum = 80;
+#ifndef BSNP_WDELTA
+#define BSNP_WDELTA 160
+#endif
+constexpr uint32_t kWDeltaNum = BSNP_WDELTA;
 constexpr int kWBins = 16384;           // label LUT bins over mu +- 2 sd
 constexpr uint32_t kLutN = 0x40u;       // LUT bit: the bin meets some [F_k - delta, F_k + delta]
 
@@ -123,7 +128,7 @@ __device__ __forceinline__ void grid_unit(const QPlan& P, uint32_t u, double m0,
       f = __double2float_rd(b64);
       r = __double2float_rn(b64);
       // a window narrower than a few f32 spacings at F would miss pred/succ
-      // of large units (2^30 elements: 80 sd / n is below one ulp of F)
+      // of large units (2^30 elements: 160 sd / n is below one ulp of F)
       const float af = fabsf(f);
       if (isfinite(af)) atomicMax(reinterpret_cast<int*>(&s_delta),
                                   __float_as_int(4.0f * (nextafterf(af, INFINITY) - af)));
