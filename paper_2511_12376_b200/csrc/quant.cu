@@ -497,12 +497,20 @@ __device__ __forceinline__ void minmax_loop(const LabelLut& L, const float* src,
   uint32_t done = 0;
   if (((uintptr_t)src & 15) == 0) {
     const uint32_t nv = size / 4;
-    for (uint32_t i = threadIdx.x; i < nv; i += kQThreads) {
-      const float4 v = ld_stream_f4(src + 4 * i);
-      visit(v.x);
-      visit(v.y);
-      visit(v.z);
-      visit(v.w);
+    constexpr int kB = 4;  // vectors per thread in flight (a tile is 8 per thread)
+    for (uint32_t i0 = threadIdx.x; i0 < nv; i0 += kB * kQThreads) {
+      float4 vb[kB];
+#pragma unroll
+      for (int b = 0; b < kB; ++b)
+        if (i0 + b * kQThreads < nv) vb[b] = ld_stream_f4(src + 4 * (i0 + b * kQThreads));
+#pragma unroll
+      for (int b = 0; b < kB; ++b) {
+        if (i0 + b * kQThreads >= nv) break;
+        visit(vb[b].x);
+        visit(vb[b].y);
+        visit(vb[b].z);
+        visit(vb[b].w);
+      }
     }
     done = nv * 4;
   }
