@@ -657,7 +657,7 @@ __global__ void __launch_bounds__(kThreads)
   const int tid = threadIdx.x;
   // n_c from the device (the encode's status word: no host round trip) or
   // by value
-  const uint64_t n_c = nc_dev ? *nc_dev : n_c_arg;
+  const uint64_t n_c = nc_dev ? min(*nc_dev, n) : n_c_arg;  // a device count is not trusted
   const uint64_t nfull = n / kTile;
   const uint64_t ntiles = (n + kTile - 1) / kTile;
   const uintptr_t p_lo = ((uintptr_t)payload + 15) & ~(uintptr_t)15;
