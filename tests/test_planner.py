@@ -197,3 +197,38 @@ def test_manifest_json_byte_identical(checkpoint_golden):
     with pytest.raises(StoreError, match="codec"):
         CheckpointManifest(iteration=3, kind="base", base_iteration=3,
                            tensors=(ManifestEntry("w", "model", "QUANT", 0, 1),))
+
+
+def _rows_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # rank r holds global ids r, r + world (one row as a list, one as a tensor)
+        rows_list = [(rank, 1, 10 + rank, 100 + rank)]
+        rows_t = torch.tensor([[rank + world, 2, 20 + rank, 200 + rank]], dtype=torch.int64)
+        a = P.exchange_sizes(rows_list, world, 2)
+        b = P.exchange_sizes(rows_t, world, 2)
+        q.put((rank, a.tolist(), b.tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_exchange_sizes_accepts_device_style_tensor_rows():
+    """The size rows may be a tensor (the bench builds them on the GPU from
+    the encoder's status word): same all-gather, same padding, at world 2."""
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_rows_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, a, b in res:
+        assert a == [[0, 1, 10, 100], [-1, -1, -1, -1], [1, 1, 11, 101], [-1, -1, -1, -1]]
+        assert b == [[2, 2, 20, 200], [-1, -1, -1, -1], [3, 2, 21, 201], [-1, -1, -1, -1]]
+    # without a process group: the local rows, padded
+    t = P.exchange_sizes(torch.tensor([[0, 1, 5, 9]]), 1, 3)
+    assert t.tolist() == [[0, 1, 5, 9], [-1, -1, -1, -1], [-1, -1, -1, -1]]
