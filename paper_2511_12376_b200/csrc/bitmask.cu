@@ -837,8 +837,8 @@ __global__ void __launch_bounds__(kThreads)
 // payload position.  The tile's payload run is contiguous, so the warp
 // stages it in shared memory with coalesced 4-byte loads (one round trip
 // instead of a dependent 2-byte load per changed element), then each lane
-// scatters its values.  The next tile's mask and offset are loaded before
-// the current one is applied.  Runs after delta_offsets_kernel validated the
+// scatters its values; mask, offsets and short payload runs are fetched two
+// / one tiles ahead (see the loop).  Runs after delta_offsets_kernel validated the
 // mask (never when a flag is raised: a corrupt record leaves the base
 // untouched).
 constexpr uint32_t kApplyStage = 1024;  // staged payload elements per warp
@@ -855,8 +855,16 @@ __global__ void __launch_bounds__(kThreads)
   const uint64_t nbytes = (n + 7) / 8;
   const bool mvec = ((uintptr_t)mask & 15) == 0;
   uint16_t* sp = stage[warp];
+  const uint64_t nfull = n / kTile;  // tiles whose every element is < n
   auto load_mask = [&](uint64_t tile, uint32_t (&w)[8]) {
     const uint64_t b0 = tile * kMaskBytes + 32 * (uint64_t)lane;
+    if (mvec && tile < nfull) {  // the common case: no bits past n to clear
+      const uint4 a = __ldg(reinterpret_cast<const uint4*>(mask + b0));
+      const uint4 b = __ldg(reinterpret_cast<const uint4*>(mask + b0 + 16));
+      w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+      w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+      return;
+    }
     if (mvec && b0 + 32 <= nbytes) {
       const uint4 a = __ldg(reinterpret_cast<const uint4*>(mask + b0));
       const uint4 b = __ldg(reinterpret_cast<const uint4*>(mask + b0 + 16));
@@ -890,44 +898,54 @@ __global__ void __launch_bounds__(kThreads)
     if (pal && e + 1 < n_c) return __ldg(reinterpret_cast<const uint32_t*>(payload + e));
     return (uint32_t)__ldg(payload + e) | (e + 1 < n_c ? (uint32_t)__ldg(payload + e + 1) << 16 : 0u);
   };
-  // the next tile's mask, offsets and (short runs) payload words are loaded
-  // while the current tile is applied
-  constexpr uint32_t kPre = 2;  // prefetched payload words per lane (runs <= 128)
-  uint32_t wn[8], pn[kPre];
-  uint64_t off_n = 0, end_n = 0;
-  auto prefetch = [&](uint64_t t) {
-    load_mask(t, wn);
-    off_n = __ldg(offsets + t);
-    end_n = __ldg(offsets + t + 1);
-    const uint64_t a0 = off_n & ~1ull;
-    const uint32_t nw = (uint32_t)((end_n - a0 + 1) / 2);
+  // a depth-2 software pipeline per warp: while tile t is applied, the mask
+  // and offsets of tile t + 2 step and the (short-run) payload words of tile
+  // t + step are in flight, so neither the mask load nor the offsets ->
+  // payload dependency is on a tile's critical path
+  constexpr uint32_t kPre = 2;  // prefetched payload words per lane (runs <= 64 words)
+  struct Slot {
+    uint32_t w[8];
+    uint64_t off, end;
+  };
+  auto load_slot = [&](uint64_t t, Slot& x) {
+    if (t < ntiles) {
+      load_mask(t, x.w);
+      x.off = __ldg(offsets + t);
+      x.end = __ldg(offsets + t + 1);
+    } else {
+      x.off = x.end = 0;
+    }
+  };
+  auto load_pre = [&](const Slot& x, uint64_t t, uint32_t (&pw)[kPre]) {
+    const uint64_t a0 = x.off & ~1ull;
+    const uint32_t nw = t < ntiles ? (uint32_t)((x.end - a0 + 1) / 2) : 0u;
 #pragma unroll
     for (uint32_t q = 0; q < kPre; ++q) {
       const uint32_t i = lane + 32 * q;
-      pn[q] = (nw <= 32 * kPre && i < nw) ? pword(a0, i) : 0u;
+      pw[q] = (nw <= 32 * kPre && i < nw) ? pword(a0, i) : 0u;
     }
   };
-  if (tile < ntiles) prefetch(tile);
+  Slot A, B;
+  uint32_t pa[kPre], pb[kPre];
+  load_slot(tile, A);
+  load_slot(tile + step, B);
+  load_pre(A, tile, pa);
   for (; tile < ntiles; tile += step) {
-    uint32_t w[8], pw[kPre];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) w[k] = wn[k];
-#pragma unroll
-    for (uint32_t q = 0; q < kPre; ++q) pw[q] = pn[q];
-    const uint64_t off = off_n, end = end_n;
-    if (tile + step < ntiles) prefetch(tile + step);
+    Slot C;
+    load_slot(tile + 2 * step, C);
+    load_pre(B, tile + step, pb);
     uint32_t c = 0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) c += __popc(w[k]);
+    for (int k = 0; k < 8; ++k) c += __popc(A.w[k]);
     const uint32_t inc = warp_inclusive_scan_u32(c, lane);
-    const uint32_t total = (uint32_t)(end - off);
-    const uint64_t a0 = off & ~1ull;
-    const uint32_t nw = (uint32_t)((end - a0 + 1) / 2);
+    const uint32_t total = (uint32_t)(A.end - A.off);
+    const uint64_t a0 = A.off & ~1ull;
+    const uint32_t nw = (uint32_t)((A.end - a0 + 1) / 2);
     const bool staged = total <= kApplyStage;
     if (nw <= 32 * kPre) {
 #pragma unroll
       for (uint32_t q = 0; q < kPre; ++q)
-        if (lane + 32 * q < nw) reinterpret_cast<uint32_t*>(sp)[lane + 32 * q] = pw[q];
+        if (lane + 32 * q < nw) reinterpret_cast<uint32_t*>(sp)[lane + 32 * q] = pa[q];
       __syncwarp();
     } else if (staged) {
       // coalesced copy of payload[off, end) into the stage
@@ -935,21 +953,36 @@ __global__ void __launch_bounds__(kThreads)
       __syncwarp();
     }
     uint32_t r = inc - c;  // rank of this lane's first change in the tile
-    const uint32_t sh = (uint32_t)(off & 1);
-    const uint64_t e0 = tile * kTile + 256 * (uint64_t)lane;
-    {
+    uint16_t* op = out + tile * kTile + 256 * (uint64_t)lane;  // this lane's elements
+    if (staged) {
+      const uint16_t* sr = sp + (uint32_t)(A.off & 1) + r;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        uint32_t b = w[k];
+        uint32_t b = A.w[k];
         while (b) {
           const uint32_t j = __ffs(b) - 1;
           b &= b - 1;
-          out[e0 + 32 * k + j] = staged ? sp[sh + r] : __ldg(payload + off + r);
-          ++r;
+          op[32 * k + j] = *sr++;
+        }
+      }
+    } else {
+      const uint16_t* pr = payload + A.off + r;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        uint32_t b = A.w[k];
+        while (b) {
+          const uint32_t j = __ffs(b) - 1;
+          b &= b - 1;
+          if (pr < payload + n_c) op[32 * k + j] = __ldg(pr);
+          ++pr;
         }
       }
     }
     __syncwarp();  // the stage is reused by the next tile
+    A = B;
+    B = C;
+#pragma unroll
+    for (uint32_t q = 0; q < kPre; ++q) pa[q] = pb[q];
   }
 }
 
