@@ -532,14 +532,33 @@ __global__ void __launch_bounds__(kEncThreads)
   }
 }
 
-// Payload offsets of every decode tile from the mask alone (n/8 bytes):
-// offsets[t] = popcount(mask[0 .. t*kTile)), offsets[ntiles] = total.  Also
-// validates padding bits and popcount == n_c (bitmask.py:128-135).  One CTA
-// per chunk of kChunkTiles tiles (128 KiB of mask), chained by a decoupled
-// look-back; each warp counts kChunkTiles / 8 tiles with kOffBatch tiles of
-// loads in flight (a tile = 1024 mask bytes = 32 lanes x 32 B).
-constexpr int kChunkTiles = 128;
-constexpr int kOffBatch = 4;
+// Payload offsets of every decode tile from the mask alone (n/8 bytes), and
+// the validation of padding bits and popcount == n_c (bitmask.py:128-135),
+// in two look-back-free launches:
+//   delta_count_kernel  one CTA per chunk of kChunkTiles tiles (all loads of
+//                       a warp's tiles in flight at once): per-tile offsets
+//                       inside the chunk (u32) and the chunk's total;
+//   delta_scan_kernel   one CTA: the exclusive scan of the chunk totals (u64
+//                       chunk bases, the total last), status->count and the
+//                       popcount check.
+// A tile's payload offset is then base[chunk] + local[tile] (TileOffsets;
+// delta_materialize_kernel writes them out as u64 for the TMA decode).
+// (A single pass chained by a decoupled look-back over 128-tile chunks took
+// 38 us at 2^30: its 1024 CTAs needed two waves at 58 registers.)
+constexpr int kChunkTiles = 32;  // 4 tiles per warp, one batch of loads
+constexpr int kChunkShift = 5;
+static_assert((1 << kChunkShift) == kChunkTiles, "chunk shift");
+constexpr int kScanThreads = 1024;
+
+struct TileOffsets {
+  const uint64_t* base;   // [nchunks + 1]: exclusive chunk bases, then the total
+  const uint32_t* local;  // [ntiles + 1]: offset of each tile inside its chunk
+  uint64_t ntiles;
+  // t <= ntiles (local[ntiles] makes at(ntiles) the total: branch-free)
+  __device__ __forceinline__ uint64_t at(uint64_t t) const {
+    return base[t >> kChunkShift] + local[t];
+  }
+};
 
 __device__ __forceinline__ uint32_t tile_lane_count(const uint8_t* __restrict__ mask, uint64_t n,
                                                     uint64_t nbytes, uint64_t b0, bool& pad) {
@@ -557,80 +576,105 @@ __device__ __forceinline__ uint32_t tile_lane_count(const uint8_t* __restrict__ 
 }
 
 __global__ void __launch_bounds__(kThreads)
-    delta_offsets_kernel(const uint8_t* __restrict__ mask, uint64_t n, uint64_t n_c,
-                         uint64_t* __restrict__ offsets, bsnp_status* __restrict__ st,
-                         uint32_t* __restrict__ ticket, uint64_t* __restrict__ chunk_status,
-                         uint64_t nchunks, const uint64_t* __restrict__ nc_dev = nullptr) {
+    delta_count_kernel(const uint8_t* __restrict__ mask, uint64_t n,
+                       uint32_t* __restrict__ local, uint32_t* __restrict__ ctot,
+                       bsnp_status* __restrict__ st) {
+  constexpr int kPerWarp = kChunkTiles / kWarps;
   __shared__ uint32_t s_cnt[kChunkTiles];
-  __shared__ uint32_t s_chunk;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_chunk = atomicAdd(ticket, 1u);
-  __syncthreads();
-  const uint64_t chunk = s_chunk;
+  const uint64_t chunk = blockIdx.x;
   const uint64_t nbytes = (n + 7) / 8;
   const uint64_t ntiles = (n + kTile - 1) / kTile;
   const bool vec = ((uintptr_t)mask & 15) == 0;
-  constexpr int kPerWarp = kChunkTiles / kWarps;
   bool pad = false;
+  uint4 a[kPerWarp], b[kPerWarp];
+  uint32_t full = 0;  // bit q: tile q is loaded whole
 #pragma unroll
-  for (int q0 = 0; q0 < kPerWarp; q0 += kOffBatch) {
-    uint4 a[kOffBatch], b[kOffBatch];
-    uint32_t full = 0;  // bit q: tile q of the batch is loaded whole
+  for (int q = 0; q < kPerWarp; ++q) {
+    const uint64_t t = chunk * kChunkTiles + warp * kPerWarp + q;
+    const uint64_t b0 = t * kMaskBytes + (uint64_t)lane * 32;
+    if (t < ntiles && vec && b0 + 32 < nbytes) {  // the last byte goes the slow way
+      full |= 1u << q;
+      a[q] = ld_stream_v4(mask + b0);
+      b[q] = ld_stream_v4(mask + b0 + 16);
+    } else {
+      a[q] = b[q] = make_uint4(0, 0, 0, 0);
+    }
+  }
 #pragma unroll
-    for (int q = 0; q < kOffBatch; ++q) {
-      const uint64_t t = chunk * kChunkTiles + warp * kPerWarp + q0 + q;
-      const uint64_t b0 = t * kMaskBytes + (uint64_t)lane * 32;
-      if (t < ntiles && vec && b0 + 32 < nbytes) {  // the last byte goes the slow way
-        full |= 1u << q;
-        a[q] = ld_stream_v4(mask + b0);
-        b[q] = ld_stream_v4(mask + b0 + 16);
-      } else {
-        a[q] = b[q] = make_uint4(0, 0, 0, 0);
-      }
+  for (int q = 0; q < kPerWarp; ++q) {
+    const int lt = warp * kPerWarp + q;
+    const uint64_t t = chunk * kChunkTiles + lt;
+    uint32_t c = 0;
+    if ((full >> q) & 1u) {
+      c = __popc(a[q].x) + __popc(a[q].y) + __popc(a[q].z) + __popc(a[q].w) +
+          __popc(b[q].x) + __popc(b[q].y) + __popc(b[q].z) + __popc(b[q].w);
+    } else if (t < ntiles) {
+      c = tile_lane_count(mask, n, nbytes, t * kMaskBytes + (uint64_t)lane * 32, pad);
     }
 #pragma unroll
-    for (int q = 0; q < kOffBatch; ++q) {
-      const int lt = warp * kPerWarp + q0 + q;
-      const uint64_t t = chunk * kChunkTiles + lt;
-      uint32_t c = 0;
-      if ((full >> q) & 1u) {
-        c = __popc(a[q].x) + __popc(a[q].y) + __popc(a[q].z) + __popc(a[q].w) +
-            __popc(b[q].x) + __popc(b[q].y) + __popc(b[q].z) + __popc(b[q].w);
-      } else if (t < ntiles) {
-        c = tile_lane_count(mask, n, nbytes, t * kMaskBytes + (uint64_t)lane * 32, pad);
-      }
-#pragma unroll
-      for (int d = 16; d > 0; d >>= 1) c += __shfl_xor_sync(kFull, c, d);
-      if (lane == 0) s_cnt[lt] = c;
-    }
+    for (int d = 16; d > 0; d >>= 1) c += __shfl_xor_sync(kFull, c, d);
+    if (lane == 0) s_cnt[lt] = c;
   }
   if (pad) atomicOr(&st->err_flags, BSNP_ERR_PADDING);
   __syncthreads();
   if (warp == 0) {
-    // lane l scans tiles 4l .. 4l + 3
-    constexpr int kPer = kChunkTiles / 32;
-    uint32_t v[kPer], s = 0;
+    const uint32_t v = s_cnt[lane];
+    const uint32_t x = warp_inclusive_scan_u32(v, lane);
+    const uint64_t t = chunk * kChunkTiles + lane;
+    if (t <= ntiles) local[t] = x - v;  // [ntiles]: the chunk total (at(ntiles) = total)
+    if (lane == 31) ctot[chunk] = x;
+  }
+}
+
+// off[t] = base[chunk] + local[t] for t <= ntiles (the TMA decode's table)
+__global__ void __launch_bounds__(kThreads)
+    delta_materialize_kernel(const uint64_t* __restrict__ base, const uint32_t* __restrict__ local,
+                             uint64_t ntiles, uint64_t* __restrict__ off) {
+  const uint64_t t = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
+  if (t <= ntiles) off[t] = base[t >> kChunkShift] + local[t];
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+    delta_scan_kernel(const uint32_t* __restrict__ ctot, uint64_t nchunks,
+                      uint64_t* __restrict__ base, uint32_t* __restrict__ local, uint64_t ntiles,
+                      bsnp_status* __restrict__ st, uint64_t n_c,
+                      const uint64_t* __restrict__ nc_dev) {
+  __shared__ uint64_t s_warp[kScanThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t per = (nchunks + kScanThreads - 1) / kScanThreads;
+  const uint64_t lo = (uint64_t)tid * per, hi = lo + per < nchunks ? lo + per : nchunks;
+  uint64_t sum = 0;
+  for (uint64_t i = lo; i < hi; ++i) sum += __ldg(ctot + i);
+  uint64_t x = sum;  // inclusive scan over the CTA
 #pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-      v[k] = s_cnt[kPer * lane + k];
-      s += v[k];
-    }
-    const uint32_t x = warp_inclusive_scan_u32(s, lane);
-    const uint32_t total = __shfl_sync(kFull, x, 31);
-    const uint64_t excl = lookback_exclusive(chunk_status, chunk, total, lane);
-    uint64_t run = excl + x - s;
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint64_t o = __shfl_up_sync(kFull, x, d);
+    if (lane >= d) x += o;
+  }
+  if (lane == 31) s_warp[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint64_t w = s_warp[lane];
 #pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-      const uint64_t t = chunk * kChunkTiles + kPer * lane + k;
-      if (t < ntiles) offsets[t] = run;
-      run += v[k];
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint64_t o = __shfl_up_sync(kFull, w, d);
+      if (lane >= d) w += o;
     }
-    if (chunk == nchunks - 1 && lane == 0) {
-      const uint64_t pc = excl + total;
-      offsets[ntiles] = pc;
-      st->count = pc;
-      if (pc != (nc_dev ? *nc_dev : n_c)) atomicOr(&st->err_flags, BSNP_ERR_POPCOUNT);
-    }
+    s_warp[lane] = w;
+  }
+  __syncthreads();
+  uint64_t run = x - sum + (warp ? s_warp[warp - 1] : 0);
+  for (uint64_t i = lo; i < hi; ++i) {
+    base[i] = run;
+    run += __ldg(ctot + i);
+  }
+  if (tid == kScanThreads - 1) {
+    const uint64_t total = s_warp[31];
+    base[nchunks] = total;
+    if ((ntiles & (kChunkTiles - 1)) == 0) local[ntiles] = 0;  // at(ntiles) = base[nchunks]
+    st->count = total;
+    if (total != (nc_dev ? *nc_dev : n_c)) atomicOr(&st->err_flags, BSNP_ERR_POPCOUNT);
   }
 }
 
@@ -793,7 +837,7 @@ template <bool kInPlace>
 __global__ void __launch_bounds__(kThreads)
     delta_apply_kernel(const uint16_t* base, const uint8_t* __restrict__ mask,
                        const uint16_t* __restrict__ payload, uint64_t n, uint64_t n_c,
-                       uint16_t* out, const uint64_t* __restrict__ offsets,
+                       uint16_t* out, const TileOffsets offsets,
                        const bsnp_status* __restrict__ st) {
   __shared__ uint64_t s_warp[kWarps];
   __shared__ uint32_t s_off[kVec][kWarps];
@@ -813,7 +857,7 @@ __global__ void __launch_bounds__(kThreads)
     cnt[j] = __popc(m);
   }
   tile_local_scan(cnt, off, s_warp, s_off);
-  const uint64_t poff = offsets[tile];
+  const uint64_t poff = offsets.at(tile);
 #pragma unroll
   for (int j = 0; j < kVec; ++j) {
     const uint32_t b = bits[j];
@@ -838,7 +882,7 @@ __global__ void __launch_bounds__(kThreads)
 // stages it in shared memory with coalesced 4-byte loads (one round trip
 // instead of a dependent 2-byte load per changed element), then each lane
 // scatters its values; mask, offsets and short payload runs are fetched two
-// / one tiles ahead (see the loop).  Runs after delta_offsets_kernel validated the
+// / one tiles ahead (see the loop).  Runs after delta_count / delta_scan validated the
 // mask (never when a flag is raised: a corrupt record leaves the base
 // untouched).
 constexpr uint32_t kApplyStage = 1024;  // staged payload elements per warp
@@ -846,7 +890,7 @@ constexpr uint32_t kApplyStage = 1024;  // staged payload elements per warp
 __global__ void __launch_bounds__(kThreads)
     delta_apply_warp_kernel(const uint8_t* __restrict__ mask,
                             const uint16_t* __restrict__ payload, uint64_t n, uint64_t n_c,
-                            uint16_t* out, const uint64_t* __restrict__ offsets,
+                            uint16_t* out, const TileOffsets offsets,
                             const bsnp_status* __restrict__ st) {
   __shared__ __align__(16) uint16_t stage[kWarps][kApplyStage + 8];
   if (*(volatile const uint32_t*)&st->err_flags) return;
@@ -910,8 +954,8 @@ __global__ void __launch_bounds__(kThreads)
   auto load_slot = [&](uint64_t t, Slot& x) {
     if (t < ntiles) {
       load_mask(t, x.w);
-      x.off = __ldg(offsets + t);
-      x.end = __ldg(offsets + t + 1);
+      x.off = offsets.at(t);
+      x.end = offsets.at(t + 1);
     } else {
       x.off = x.end = 0;
     }
@@ -1060,11 +1104,50 @@ extern "C" size_t bsnp_delta_encode_ws_bytes(uint64_t n) {
   return enc_scratch_offset(n) + 2 * (size_t)enc_slots(n, nullptr) * kTile + 256;
 }
 
+// decode workspace: ticket header | chunk bases u64 [nchunks + 1] | tile
+// offsets inside their chunk u32 [ntiles + 1] | chunk totals u32 [nchunks]
+struct DecWs {
+  uint32_t* ticket;
+  uint64_t* base;
+  uint32_t* local;
+  uint32_t* ctot;
+  uint64_t* off;
+  uint64_t nchunks;
+};
+static DecWs dec_ws(void* ws, uint64_t n) {
+  DecWs w;
+  const uint64_t nt = num_tiles(n);
+  w.nchunks = (nt + kChunkTiles - 1) / kChunkTiles;
+  w.ticket = (uint32_t*)ws;
+  w.base = (uint64_t*)((char*)ws + kWsHeader);
+  w.local = (uint32_t*)(w.base + w.nchunks + 1);
+  w.ctot = w.local + nt + 1;
+  w.off = (uint64_t*)(((uintptr_t)(w.ctot + w.nchunks) + 7) & ~(uintptr_t)7);
+  return w;
+}
+
 extern "C" size_t bsnp_delta_decode_ws_bytes(uint64_t n) {
-  // ticket | chunk status words | tile payload offsets [ntiles + 1]
   const uint64_t nt = num_tiles(n);
   const uint64_t nchunks = (nt + kChunkTiles - 1) / kChunkTiles;
-  return kWsHeader + 8 * (size_t)nchunks + 8 * (size_t)(nt + 1);
+  return kWsHeader + 8 * (size_t)(nchunks + 1) + 4 * (size_t)(nt + 1) + 4 * (size_t)nchunks + 8 +
+         8 * (size_t)(nt + 1);
+}
+
+// the offsets + validation launches of a decode (n > 0)
+// materialize: also the u64 offsets array the TMA decode reads (measured:
+// its refill reading base + local directly ran 0.84 instead of 0.71 ms)
+static int launch_offsets(const uint8_t* mask, uint64_t n, uint64_t n_c, const uint64_t* nc_dev,
+                          const DecWs& w, bsnp_status* status, cudaStream_t s, bool materialize) {
+  delta_count_kernel<<<(unsigned)w.nchunks, kThreads, 0, s>>>(mask, n, w.local, w.ctot, status);
+  int rc = launch_status("delta_count_kernel");
+  if (rc) return rc;
+  delta_scan_kernel<<<1, kScanThreads, 0, s>>>(w.ctot, w.nchunks, w.base, w.local,
+                                                num_tiles(n), status, n_c, nc_dev);
+  rc = launch_status("delta_scan_kernel");
+  if (rc || !materialize) return rc;
+  delta_materialize_kernel<<<(unsigned)((num_tiles(n) + kThreads) / kThreads), kThreads, 0, s>>>(
+      w.base, w.local, num_tiles(n), w.off);
+  return launch_status("delta_materialize_kernel");
 }
 
 extern "C" int bsnp_delta_encode(const uint16_t* base, const uint16_t* target, uint64_t n,
@@ -1116,26 +1199,23 @@ extern "C" int bsnp_delta_decode(const uint16_t* base, const uint8_t* mask,
   int rc = cuda_status("memset(status)", cudaMemsetAsync(status, 0, sizeof(bsnp_status), s));
   if (rc || n == 0) return rc;
   const uint64_t nt = num_tiles(n);
-  const uint64_t nchunks = (nt + kChunkTiles - 1) / kChunkTiles;
-  uint32_t* ticket = (uint32_t*)ws;
-  uint32_t* ticket2 = (uint32_t*)ws + 32;
-  uint64_t* cstat = (uint64_t*)((char*)ws + kWsHeader);
-  uint64_t* offsets = cstat + nchunks;
-  rc = cuda_status("memset(ws)", cudaMemsetAsync(ws, 0, kWsHeader + 8 * nchunks, s));
+  const DecWs w = dec_ws(ws, n);
+  uint32_t* ticket2 = w.ticket + 32;
+  const TileOffsets offsets{w.base, w.local, nt};
+  rc = cuda_status("memset(ws)", cudaMemsetAsync(ws, 0, kWsHeader, s));
   if (rc) return rc;
-  // pass 1: payload offsets per tile + validation (reads n/8 bytes)
-  delta_offsets_kernel<<<(unsigned)nchunks, kThreads, 0, s>>>(mask, n, n_c, offsets, status,
-                                                              ticket, cstat, nchunks);
-  if ((rc = launch_status("delta_offsets_kernel"))) return rc;
   const bool in_place = (const void*)base == (const void*)out;
   const bool aligned = (((uintptr_t)base | (uintptr_t)out | (uintptr_t)mask) & 15) == 0;
+  const bool tma = aligned && (!in_place || n_c * 32 > n);
+  // pass 1: payload offsets per tile + validation (reads n/8 bytes)
+  if ((rc = launch_offsets(mask, n, n_c, nullptr, w, status, s, tma))) return rc;
   if (in_place && aligned && n_c * 32 > n) {
     // dense: streaming the whole tile beats touching the changed words
     // (p = 25 %: 0.77 vs 1.27 ms at 2^30)
     const size_t smem = (size_t)kDecStages * kDecStage;
     auto k = delta_decode_tma_kernel<kDecStages, true>;
     const int grid = persistent_grid(k, smem, nt);
-    k<<<grid, kThreads, smem, s>>>(base, mask, payload, n, n_c, out, offsets, ticket2, status,
+    k<<<grid, kThreads, smem, s>>>(base, mask, payload, n, n_c, out, w.off, ticket2, status,
                                    nullptr);
   } else if (in_place) {
     const int sms = device_sms();
@@ -1150,7 +1230,7 @@ extern "C" int bsnp_delta_decode(const uint16_t* base, const uint8_t* mask,
     auto k = n_c * 32 > n ? delta_decode_tma_kernel<kDecStages, true>
                           : delta_decode_tma_kernel<kDecStages, false>;
     const int grid = persistent_grid(k, smem, nt);
-    k<<<grid, kThreads, smem, s>>>(base, mask, payload, n, n_c, out, offsets, ticket2, nullptr,
+    k<<<grid, kThreads, smem, s>>>(base, mask, payload, n, n_c, out, w.off, ticket2, nullptr,
                                    nullptr);
   } else {
     delta_apply_kernel<false><<<(unsigned)nt, kThreads, 0, s>>>(base, mask, payload, n, n_c,
@@ -1173,23 +1253,19 @@ extern "C" int bsnp_delta_decode_dn(const uint16_t* base, const uint8_t* mask,
   int rc = cuda_status("memset(status)", cudaMemsetAsync(status, 0, sizeof(bsnp_status), s));
   if (rc || n == 0) return rc;
   const uint64_t nt = num_tiles(n);
-  const uint64_t nchunks = (nt + kChunkTiles - 1) / kChunkTiles;
-  uint32_t* ticket = (uint32_t*)ws;
-  uint32_t* ticket2 = (uint32_t*)ws + 32;
-  uint64_t* cstat = (uint64_t*)((char*)ws + kWsHeader);
-  uint64_t* offsets = cstat + nchunks;
-  rc = cuda_status("memset(ws)", cudaMemsetAsync(ws, 0, kWsHeader + 8 * nchunks, s));
+  const DecWs w = dec_ws(ws, n);
+  uint32_t* ticket2 = w.ticket + 32;
+  const TileOffsets offsets{w.base, w.local, nt};
+  rc = cuda_status("memset(ws)", cudaMemsetAsync(ws, 0, kWsHeader, s));
   if (rc) return rc;
-  delta_offsets_kernel<<<(unsigned)nchunks, kThreads, 0, s>>>(mask, n, 0, offsets, status,
-                                                              ticket, cstat, nchunks, n_c_dev);
-  if ((rc = launch_status("delta_offsets_kernel"))) return rc;
+  if ((rc = launch_offsets(mask, n, 0, n_c_dev, w, status, s, true))) return rc;
   const bool aligned = (((uintptr_t)base | (uintptr_t)out | (uintptr_t)mask) & 15) == 0;
   if (aligned) {
     // the sparse (bit-walk) expansion: n_c is not known on the host
     const size_t smem = (size_t)kDecStages * kDecStage;
     auto k = delta_decode_tma_kernel<kDecStages, false>;
     const int grid = persistent_grid(k, smem, nt);
-    k<<<grid, kThreads, smem, s>>>(base, mask, payload, n, 0, out, offsets, ticket2, nullptr,
+    k<<<grid, kThreads, smem, s>>>(base, mask, payload, n, 0, out, w.off, ticket2, nullptr,
                                    n_c_dev);
     return launch_status("delta_decode_kernel");
   }

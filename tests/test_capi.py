@@ -46,7 +46,9 @@ def test_ws_sizes_without_gpu():
         head = -(-(256 + 8 * nt) // 256) * 256
         slots = min(nt, 16) if nt > 16 else nt
         assert lib.bsnp_delta_encode_ws_bytes(n) == head + 16384 * slots + 256
-        assert lib.bsnp_delta_decode_ws_bytes(n) == 256 + 8 * -(-nt // 128) + 8 * (nt + 1)
+        nch = -(-nt // 32)
+        assert lib.bsnp_delta_decode_ws_bytes(n) == (256 + 8 * (nch + 1) + 4 * (nt + 1) + 4 * nch
+                                                     + 8 + 8 * (nt + 1))
 
 
 def test_argument_errors_without_gpu():
