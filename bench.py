@@ -486,7 +486,7 @@ def run_b200(args, rank: int, world: int, local_rank: int):
                      "algorithmic_bytes": dom_bytes,
                      "traffic": traffic["bytes"] if traffic else None,
                      "traffic_detail": traffic},
-        "gpu_launches": 3 * args.steps,  # encode, offsets, decode per step
+        "gpu_launches": 5 * args.steps,  # encode; count, scan, offsets table, decode per step
         "clocks": clk,
     }
     if e2e:
