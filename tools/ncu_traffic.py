@@ -13,7 +13,8 @@ import sys
 
 GROUPS = {
     "delta_encode": ["delta_encode_ws_kernel"],
-    "delta_decode": ["delta_count_kernel", "delta_scan_kernel", "delta_decode_tma_kernel<2, 0>"],
+    "delta_decode": ["delta_count_kernel", "delta_scan_kernel", "delta_materialize_kernel",
+                     "delta_decode_tma_kernel<2, 0>"],
     "cluster_encode": ["fit_sum_kernel", "fit_stats_kernel", "fit_var_fallback_kernel",
                        "fit_var_combine_kernel", "fit_label_kernel",
                        "fit_decide_kernel", "fit_minmax_kernel", "fit_finalize_kernel",
