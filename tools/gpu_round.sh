@@ -17,7 +17,7 @@ timeout 300 $CMD > gpurun_out/plain_$tag.log 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file gpurun_out/launches_$tag.csv $CMD > gpurun_out/ncu_launch_$tag.log 2>&1 && \
   timeout 1500 ncu --set full --clock-control none --import-source on \
-    -k "regex:delta_(encode_ws|decode_tma|offsets)|fit_sum|fit_label|quantize_codes|dequantize_kernel" -c 8 -f -o gpurun_out/prof_$tag $CMD \
+    -k "regex:delta_(encode_ws|decode_tma|count|scan)|fit_sum|fit_label|quantize_codes|dequantize_kernel" -c 8 -f -o gpurun_out/prof_$tag $CMD \
     > gpurun_out/ncu_full_$tag.log 2>&1
   # the cluster encode / dequantize kernels of one C2 encode + dequantize
   timeout 300 python tools/lab_quant_once.py > gpurun_out/plainq_$tag.log 2>&1 && \
