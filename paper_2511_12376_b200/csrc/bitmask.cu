@@ -886,6 +886,9 @@ __global__ void __launch_bounds__(kThreads)
 // mask (never when a flag is raised: a corrupt record leaves the base
 // untouched).
 constexpr uint32_t kApplyStage = 1024;  // staged payload elements per warp
+#ifndef BSNP_COOP_SCATTER
+#define BSNP_COOP_SCATTER 1
+#endif
 
 __global__ void __launch_bounds__(kThreads)
     delta_apply_warp_kernel(const uint8_t* __restrict__ mask,
@@ -998,7 +1001,43 @@ __global__ void __launch_bounds__(kThreads)
     }
     uint32_t r = inc - c;  // rank of this lane's first change in the tile
     uint16_t* op = out + tile * kTile + 256 * (uint64_t)lane;  // this lane's elements
-    if (staged) {
+    if (staged && BSNP_COOP_SCATTER) {
+      // warp-cooperative scatter: lane l writes the changes of rank l, l +
+      // 32, ... of the tile (not its own lane's), so the warp runs
+      // ceil(total / 32) rounds instead of a loop per mask word paced by
+      // its busiest lane.  Rank q's owner lane is the first whose inclusive
+      // count exceeds q (binary search by shuffles); its 8 mask words come
+      // over by shuffles and the q-th set bit is found word by word.
+      const uint32_t ex = inc - c;
+      const uint16_t* sr = sp + (uint32_t)(A.off & 1);
+      uint16_t* tp = out + tile * kTile;
+      for (uint32_t r0 = 0; r0 < total; r0 += 32) {
+        const uint32_t q = r0 + lane;
+        uint32_t L = 0;
+#pragma unroll
+        for (uint32_t st = 16; st > 0; st >>= 1)
+          if (__shfl_sync(kFull, inc, L + st - 1) <= q) L += st;
+        uint32_t lq = q - __shfl_sync(kFull, ex, L);  // rank inside lane L
+        uint32_t word = 0, kk = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t wk = __shfl_sync(kFull, A.w[k], L);
+          const uint32_t pc = __popc(wk);
+          const bool here = kk == 0 && lq < pc;  // first word holding rank lq
+          if (here) {
+            word = wk;
+            kk = (uint32_t)k + 1;
+          } else if (kk == 0) {
+            lq -= pc;
+          }
+        }
+        if (q < total) {
+          for (uint32_t i = 0; i < lq; ++i) word &= word - 1;
+          const uint32_t j = __ffs(word) - 1;
+          tp[256 * L + 32 * (kk - 1) + j] = sr[q];
+        }
+      }
+    } else if (staged) {
       const uint16_t* sr = sp + (uint32_t)(A.off & 1) + r;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
@@ -1255,7 +1294,6 @@ extern "C" int bsnp_delta_decode_dn(const uint16_t* base, const uint8_t* mask,
   const uint64_t nt = num_tiles(n);
   const DecWs w = dec_ws(ws, n);
   uint32_t* ticket2 = w.ticket + 32;
-  const TileOffsets offsets{w.base, w.local, nt};
   rc = cuda_status("memset(ws)", cudaMemsetAsync(ws, 0, kWsHeader, s));
   if (rc) return rc;
   if ((rc = launch_offsets(mask, n, 0, n_c_dev, w, status, s, true))) return rc;
