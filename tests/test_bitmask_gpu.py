@@ -314,3 +314,27 @@ def test_decode_with_device_count(dev, n, p):
     (pc, f1), = rt.read_status(st[1:2])
     with pytest.raises(B.DeltaError, match="popcount"):
         B._raise_decode_flags(f1, pc, idx.size + 1)
+
+
+@pytest.mark.parametrize("n,p,clustered", [(5 * 8192 + 77, 0.005, False), (5 * 8192 + 77, 0.03, False),
+                                           ((1 << 20) + 11, 0.0625, False),
+                                           (3 * 8192 + 5, 0.02, True)])
+def test_in_place_apply_sparse_rounds(dev, n, p, clustered):
+    """Sparse chain replay (warp-cooperative scatter: lane l writes the
+    changes of rank l, l + 32, ... of a tile) over tiles with one and several
+    rounds of 32 changes, and with a tile whose changes all sit in one lane's
+    256 elements, equals the oracle's decode."""
+    from paper_2511_12376_b200 import bitmask as B
+    rng = np.random.default_rng(int(n * p) + clustered)
+    base = rng.integers(0, 1 << 16, n, dtype=np.uint16)
+    cur = base.copy()
+    k = int(round(p * n))
+    if clustered:
+        idx = 8192 + 256 * 5 + rng.choice(256, min(k, 200), replace=False)  # one lane of tile 1
+    else:
+        idx = rng.choice(n, k, replace=False)
+    cur[idx] ^= rng.integers(1, 1 << 16, idx.size, dtype=np.uint16)
+    d = B.encode_delta_device(_dev_u16(base, dev), _dev_u16(cur, dev))
+    bt = _dev_u16(base, dev)
+    B.decode_delta_device(bt, d.mask, d.payload, d.n_c, out=bt)
+    assert np.array_equal(bt.cpu().numpy().view(np.uint16), cur)
