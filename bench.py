@@ -747,6 +747,26 @@ def run_ckpt_sharded(config, dev, rank, world, reps: int = 2):
                 for sp in (specs[i] for i in mine)) + 512 * (len(mine) + 1)
     import numpy as np
     from paper_2511_12376_b200 import _runtime as rt
+    # two registered landing buffers per rank: check the node's free host
+    # memory first (every rank must agree, or the collectives below hang)
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = None
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+    need = 2 * bound * local_world
+    ok = torch.tensor([1 if (avail is None or need < 0.85 * avail) else 0], dtype=torch.int64)
+    if world > 1:
+        if dist.get_backend() == "nccl":
+            ok = ok.to(dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if int(ok.item()) == 0:
+        del c0, c1, loc0, loc1, prev, enc
+        torch.cuda.empty_cache()
+        return {"key": f"{config.lower()}_sharded",
+                "skipped": f"host memory: {need / 1e9:.0f} GB of landing buffers for "
+                           f"{local_world} rank(s), {(avail or 0) / 1e9:.0f} GB available"}
     host = [np.empty(bound, dtype=np.uint8) for _ in range(2)]
     for a in host:   # page-locked by registration (the caching allocator rounds up to 2^k)
         assert rt.lib().bsnp_host_register(a.ctypes.data, bound) == 0, "host register failed"
