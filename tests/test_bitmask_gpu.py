@@ -36,7 +36,7 @@ def test_golden_records_byte_identical(dev, bitmask_golden, golden_index):
 
 
 @pytest.mark.parametrize("n", [1, 5, 8, 13, 255, 8191, 8192, 8193, 3 * 8192 + 5,
-                               32768 * 33 + 7, (1 << 20) + 3])
+                               32 * 8192, 64 * 8192 + 1, 32768 * 33 + 7, (1 << 20) + 3])
 @pytest.mark.parametrize("frac", [0.0, 0.001, 0.1, 0.5, 1.0])
 def test_device_encode_decode_vs_oracle(dev, n, frac):
     from paper_2511_12376_b200 import bitmask as B
