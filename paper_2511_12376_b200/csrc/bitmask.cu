@@ -889,6 +889,9 @@ constexpr uint32_t kApplyStage = 1024;  // staged payload elements per warp
 #ifndef BSNP_DENSE_DIV
 #define BSNP_DENSE_DIV 16  // in place: n_c > n / DIV streams whole tiles (TMA decode); 6.25 %: 0.667 sparse vs 0.697 ms dense
 #endif
+#ifndef BSNP_APPLY_CTAS_PER_SM
+#define BSNP_APPLY_CTAS_PER_SM 32  // more, shorter CTAs balance better (p = 6.25 %: 0.652 -> 0.600 ms)
+#endif
 #ifndef BSNP_COOP_SCATTER
 #define BSNP_COOP_SCATTER 1
 #endif
@@ -1264,7 +1267,8 @@ extern "C" int bsnp_delta_decode(const uint16_t* base, const uint8_t* mask,
     // one warp per tile, a few tiles per warp
     const uint64_t warps = (nt + 3) / 4;
     const uint64_t want = (warps + kWarps - 1) / kWarps;
-    const uint64_t grid = want < (uint64_t)sms * 8 ? want : (uint64_t)sms * 8;
+    const uint64_t cap = (uint64_t)sms * BSNP_APPLY_CTAS_PER_SM;
+    const uint64_t grid = want < cap ? want : cap;
     delta_apply_warp_kernel<<<(unsigned)(grid ? grid : 1), kThreads, 0, s>>>(
         mask, payload, n, n_c, out, offsets, status);
   } else if (aligned) {
