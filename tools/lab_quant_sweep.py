@@ -1,5 +1,5 @@
 """Quantizer lab: build a variant of _bsnp.so with EXTRA nvcc flags (e.g.
-"-DBSNP_WDELTA=160") and time the C2 encode / dequantize (Adam-m and Adam-v,
+"-DBSNP_WDELTA=160") and time the C2 encode and dequantize (Adam-m and Adam-v,
 per 2^20 block and per tensor; CUDA events, 5 reps) — dev tool."""
 import os, sys
 sys.path.insert(0, os.getcwd())
@@ -27,7 +27,17 @@ for dist in ("adam_m", "adam_v"):
         for _ in range(5):
             Q.cluster_encode_async(x, 16, block, tables, labels, codes)
         e1.record(); torch.cuda.synchronize()
-        print(f"{tag} {dist} block={block or 'tensor'}: encode {e0.elapsed_time(e1) / 5:.4f} ms",
-              flush=True)
-        del tables, labels, codes
+        te = e0.elapsed_time(e1) / 5
+        out = torch.empty_like(x)
+        st = torch.zeros(4, dtype=torch.int64, device=dev)
+        for _ in range(2):
+            Q.cluster_dequantize_async(labels, codes, n, block, tables, out, st)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(5):
+            Q.cluster_dequantize_async(labels, codes, n, block, tables, out, st)
+        e1.record(); torch.cuda.synchronize()
+        print(f"{tag} {dist} block={block or 'tensor'}: encode {te:.4f} ms | dequantize "
+              f"{e0.elapsed_time(e1) / 5:.4f} ms", flush=True)
+        del tables, labels, codes, out
     del x
