@@ -52,7 +52,10 @@ struct QPlan {
   uint64_t total_tiles;
   uint32_t nunits, m;
   uint32_t D_full, T_full;  // tree depth / tiles of a full unit
-  uint32_t D_last, T_last;  // of the last unit
+  uint32_t D_last, T_last;  // of the last unit (T_last may exceed T_full: numpy's
+                            // splits of a slightly shorter length can leave a
+                            // piece above kTileMax one level deeper)
+  uint32_t D_max, T_max;    // max of the two: per-unit enumerations use T_max
   uint32_t C_full, C_last;  // dequantize chunks per unit
 };
 
@@ -394,7 +397,8 @@ __device__ __forceinline__ void combine_unit(const QPlan& P, uint32_t u,
   // (pre_combine_kernel): the same perfect tree, one level set at a time
   const int sh = T > kPreGroup ? kPreShift : 0;
   const uint32_t Tg = T >> sh;
-  const double S = combine_perfect((sh ? partials2 : partials) + ((uint64_t)u * P.T_full >> sh),
+  const double S = combine_perfect(sh ? partials2 + (uint64_t)u * (P.T_max >> kPreShift)
+                                      : partials + (uint64_t)u * P.T_full,
                                    Tg, sv);
   if (threadIdx.x != 0) return;
   const double mean = __ddiv_rn(__dadd_rn(0.0, S), (double)len);  // np.mean
@@ -444,12 +448,13 @@ __global__ void __launch_bounds__(kQThreads)
     pre_combine_kernel(QPlan P, const double* __restrict__ partials,
                        double* __restrict__ partials2) {
   __shared__ double v[kPreGroup];
-  const uint64_t g = blockIdx.x;  // group index over all units (T_full-strided)
-  const uint64_t gpu = P.T_full >> kPreShift;  // groups per full unit
+  const uint64_t g = blockIdx.x;  // group index over all units (T_max-strided)
+  const uint64_t gpu = P.T_max >> kPreShift;  // group slots per unit
   const uint32_t u = (uint32_t)(g / gpu);
   const uint32_t T = u == P.nunits - 1 ? P.T_last : P.T_full;
-  if (((g % gpu) << kPreShift) >= T) return;  // the last unit may have fewer tiles
-  const double* src = partials + (g << kPreShift);
+  const uint64_t gi = g % gpu;
+  if ((gi << kPreShift) >= T) return;  // units with fewer tiles
+  const double* src = partials + (uint64_t)u * P.T_full + (gi << kPreShift);
   for (int i = threadIdx.x; i < (int)kPreGroup; i += kQThreads) v[i] = src[i];
   constexpr int kPer = kPreGroup / 2 / kQThreads;  // pairs per thread at the first level
   for (uint32_t w = kPreGroup / 2; w >= 1; w /= 2) {
@@ -1073,6 +1078,8 @@ bool make_plan(uint64_t n, uint64_t block, int m, QPlan& P) {
   P.T_full = 1u << P.D_full;
   P.D_last = tree_depth(P.last_len);
   P.T_last = 1u << P.D_last;
+  P.D_max = P.D_full > P.D_last ? P.D_full : P.D_last;
+  P.T_max = 1u << P.D_max;
   P.total_tiles = (uint64_t)(P.nunits - 1) * P.T_full + P.T_last;
   P.C_full = (uint32_t)((b + kDqChunk - 1) / kDqChunk);
   P.C_last = (uint32_t)((P.last_len + kDqChunk - 1) / kDqChunk);
@@ -1082,7 +1089,7 @@ bool make_plan(uint64_t n, uint64_t block, int m, QPlan& P) {
 struct UGrid;
 struct QWs {
   double* partials;  // total_tiles
-  double* partials2; // nunits * (T_full / kPreGroup): pre-reduced partials (T_full > kPreGroup)
+  double* partials2; // nunits * (T_max / kPreGroup): pre-reduced partials (T > kPreGroup)
   double* mu;        // nunits
   float* fthr;       // nunits * 16
   int* tile_mm;      // total_tiles * 32
@@ -1105,7 +1112,7 @@ QWs carve(const QPlan& P, void* ws) {
     return r;
   };
   w.partials = (double*)take(8 * P.total_tiles);
-  w.partials2 = (double*)take(8 * (size_t)P.nunits * (P.T_full >> kPreShift) + 8);
+  w.partials2 = (double*)take(8 * (size_t)P.nunits * (P.T_max >> kPreShift) + 8);
   w.mu = (double*)take(8 * (size_t)P.nunits);
   w.fthr = (float*)take(64 * (size_t)P.nunits);
   w.tile_mm = (int*)take(128 * P.total_tiles);
@@ -1113,7 +1120,7 @@ QWs carve(const QPlan& P, void* ws) {
   w.ug = (UGrid*)take(kUGridBytes * (size_t)P.nunits);
   w.need = (uint32_t*)take(4 * ((size_t)P.nunits + 1));
   w.partials_q = (double*)take(8 * P.total_tiles);
-  w.partials2_q = (double*)take(8 * (size_t)P.nunits * (P.T_full >> kPreShift) + 8);
+  w.partials2_q = (double*)take(8 * (size_t)P.nunits * (P.T_max >> kPreShift) + 8);
   w.list = (uint32_t*)take(4 * ((size_t)P.nunits + 1));
   w.bytes = o;
   return w;
@@ -1125,8 +1132,8 @@ template <bool kVar>
 int launch_combine(const QPlan& P, bsnp_cluster_table* tables, const QWs& w, cudaStream_t s) {
   int rc;
   const double* p2 = nullptr;
-  if (P.T_full > kPreGroup) {
-    pre_combine_kernel<<<(unsigned)(P.nunits * (P.T_full >> kPreShift)), kQThreads, 0, s>>>(
+  if (P.T_max > kPreGroup) {
+    pre_combine_kernel<<<(unsigned)(P.nunits * (P.T_max >> kPreShift)), kQThreads, 0, s>>>(
         P, w.partials, w.partials2);
     if ((rc = launch_status("pre_combine_kernel"))) return rc;
     p2 = w.partials2;
@@ -1176,8 +1183,8 @@ int run_window(const float* x, const QPlan& P, bsnp_cluster_table* tables, uint8
   // tree only for the units whose sigma interval does not decide the tables
   fit_sum_kernel<<<tiles, kQThreads, 0, s>>>(x, P, w.partials, w.partials_q, w.list);
   if ((rc = launch_status("fit_sum_kernel"))) return rc;
-  if (P.T_full > kPreGroup) {
-    pre_combine2_kernel<<<(unsigned)(2 * P.nunits * (P.T_full >> kPreShift)), kQThreads, 0, s>>>(
+  if (P.T_max > kPreGroup) {
+    pre_combine2_kernel<<<(unsigned)(2 * P.nunits * (P.T_max >> kPreShift)), kQThreads, 0, s>>>(
         P, w.partials, w.partials_q, w.partials2, w.partials2_q);
     if ((rc = launch_status("pre_combine2_kernel"))) return rc;
   }

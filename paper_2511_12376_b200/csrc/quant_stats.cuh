@@ -125,11 +125,12 @@ __global__ void __launch_bounds__(kQThreads)
   __shared__ double v[kPreGroup];
   const uint64_t g = blockIdx.x >> 1;
   const bool isq = blockIdx.x & 1;
-  const uint64_t gpu = P.T_full >> kPreShift;
+  const uint64_t gpu = P.T_max >> kPreShift;  // group slots per unit
   const uint32_t u = (uint32_t)(g / gpu);
   const uint32_t T = u == P.nunits - 1 ? P.T_last : P.T_full;
-  if (((g % gpu) << kPreShift) >= T) return;
-  const double* src = (isq ? partials_q : partials) + (g << kPreShift);
+  const uint64_t gi = g % gpu;
+  if ((gi << kPreShift) >= T) return;
+  const double* src = (isq ? partials_q : partials) + (uint64_t)u * P.T_full + (gi << kPreShift);
   for (int i = threadIdx.x; i < (int)kPreGroup; i += kQThreads) v[i] = src[i];
   constexpr int kPer = kPreGroup / 2 / kQThreads;
   for (uint32_t w = kPreGroup / 2; w >= 1; w /= 2) {
@@ -251,7 +252,7 @@ __global__ void __launch_bounds__(kQThreads)
   uint64_t len;
   unit_shape(P, u, T, len);
   const int sh = T > kPreGroup ? kPreShift : 0;
-  const uint64_t first = (uint64_t)u * P.T_full >> sh;
+  const uint64_t first = sh ? (uint64_t)u * (P.T_max >> kPreShift) : (uint64_t)u * P.T_full;
   const double S = combine_perfect((sh ? partials2 : partials) + first, T >> sh, sv);
   __syncthreads();
   const double D2 = combine_perfect((sh ? partials2_q : partials_q) + first, T >> sh, sv);
@@ -290,7 +291,9 @@ __global__ void __launch_bounds__(kQThreads)
   __shared__ Heap H;
   const uint32_t cnt = __ldcg(list);
   for (uint64_t item = blockIdx.x;; item += gridDim.x) {
-    const uint64_t i = item >> P.D_full, j = item & (P.T_full - 1);
+    // T_max tile slots per listed unit (the last unit may have more tiles
+    // than a full one)
+    const uint64_t i = item >> P.D_max, j = item & (P.T_max - 1);
     if (i >= cnt) break;
     const uint32_t u = __ldcg(list + 1 + i);
     const uint32_t T = u == P.nunits - 1 ? P.T_last : P.T_full;

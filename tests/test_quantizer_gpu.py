@@ -424,3 +424,32 @@ def test_four_pass_path_matches_window_path(dev, monkeypatch, n, block, dist, m)
     _check_units(x, m, block, b)
     for f in ("tables", "labels", "codes"):
         assert bytes(getattr(a, f).cpu().numpy()) == bytes(getattr(b, f).cpu().numpy()), f
+
+
+@pytest.mark.parametrize("n,block,dist,m,env", [
+    (15 * 32768 + 32749, 32768, "offset_big", 5, None),         # the stress-test case
+    (2 * (1 << 20) + (1 << 20) - 7, 1 << 20, "adam_m", 16, "BSNP_VAR_EXACT"),
+    (2 * (1 << 20) + (1 << 20) - 9, 1 << 20, "adam_v", 16, "BSNP_WINDOW"),
+    ((1 << 23) + (1 << 23) - 19, 1 << 23, "adam_m", 16, None),  # last unit > kPreGroup tiles
+    ((1 << 23) + (1 << 23) - 19, 1 << 23, "offset", 16, "BSNP_VAR_EXACT"),
+])
+def test_last_unit_deeper_than_full_units(dev, monkeypatch, n, block, dist, m, env):
+    """numpy's split of a slightly shorter last unit can leave a piece above
+    one tree tile and so need one more level: the last unit then has MORE
+    tiles than a full unit (e.g. 32749 elements: 8 tiles vs 4 for 32768).
+    The variance fallback, the pre-reduction of > 1024-tile units and the
+    four-pass path enumerate T_max tile slots per unit; every unit equals
+    the oracle (regression: the stress run's 'offset' case, whose units all
+    take the exact variance tree, had a wrong sigma in its last unit)."""
+    from paper_2511_12376_b200 import quantizer as Q
+    if env == "BSNP_VAR_EXACT":
+        monkeypatch.setenv("BSNP_VAR_EXACT", "1")
+    elif env == "BSNP_WINDOW":
+        monkeypatch.setenv("BSNP_WINDOW", "0")
+    rng = np.random.default_rng(n % 100003)
+    if dist == "offset_big":    # |mean| / sd ~ 1e7: sigma's interval is too wide, exact tree
+        x = (1e4 + rng.standard_normal(n) * 1e-3).astype(np.float32)
+    else:
+        x = _dist(dist, n, rng).astype(np.float32)
+    dq = Q.cluster_encode_device(_f32(x, dev), m, block)
+    _check_units(x, m, block, dq)
