@@ -54,7 +54,12 @@ while time.time() < t_end:
     n = int(rng.choice([rng.integers(1, 9000), rng.integers(9000, 1 << 20),
                         rng.integers(1 << 20, 1 << 21)]))
     m = int(rng.integers(2, 17))
-    block = int(rng.choice([0, 0, 1 << int(rng.integers(13, 20)), 8 * int(rng.integers(1000, 40000))]))
+    block = int(rng.choice([0, 0, 1 << int(rng.integers(13, 20)), 8 * int(rng.integers(1000, 40000)),
+                            8192 * int(rng.integers(1, 40))]))
+    if block and rng.random() < 0.3:
+        # a last unit a few elements short of a full one (its tree can be one
+        # level deeper than a full unit's)
+        n = block * int(rng.integers(1, 8)) + block - 8 * int(rng.integers(0, 4)) - int(rng.integers(1, 8))
     x = dist(kind, n).astype(np.float32)
     if not np.all(np.isfinite(x)):
         x = np.nan_to_num(x, posinf=3e38, neginf=-3e38).astype(np.float32)
@@ -99,7 +104,7 @@ while time.time() < t_end:
             print(f"ERROR quant kind={kind} n={n}: {e}", flush=True)
     # bitmask
     nb = int(rng.integers(0, 3_000_000))
-    p = float(rng.choice([0.0, 1e-4, 0.01, 0.2, 0.9, 1.0]))
+    p = float(rng.choice([0.0, 1e-4, 0.01, 0.03, 0.0625, 0.2, 0.9, 1.0]))
     base = rng.integers(0, 1 << 16, nb, dtype=np.uint16)
     cur = base.copy()
     k = int(nb * p)
