@@ -338,3 +338,23 @@ def test_in_place_apply_sparse_rounds(dev, n, p, clustered):
     bt = _dev_u16(base, dev)
     B.decode_delta_device(bt, d.mask, d.payload, d.n_c, out=bt)
     assert np.array_equal(bt.cpu().numpy().view(np.uint16), cur)
+
+
+def test_in_place_apply_sparse_record_with_a_dense_tile(dev):
+    """A sparse record (n_c <= n/16: the per-warp apply) whose one tile holds
+    more changes than the warp's shared-memory stage (> 1024): that tile's
+    payload is read from global memory; the rest is staged."""
+    from paper_2511_12376_b200 import bitmask as B
+    rng = np.random.default_rng(17)
+    n = 40 * 8192 + 123
+    base = rng.integers(0, 1 << 16, n, dtype=np.uint16)
+    cur = base.copy()
+    idx = np.concatenate([8192 * 7 + rng.choice(8192, 5000, replace=False),  # one dense tile
+                          rng.choice(n, 3000, replace=False)])
+    idx = np.unique(idx)
+    cur[idx] ^= rng.integers(1, 1 << 16, idx.size, dtype=np.uint16)
+    assert idx.size * 16 <= n
+    d = B.encode_delta_device(_dev_u16(base, dev), _dev_u16(cur, dev))
+    bt = _dev_u16(base, dev)
+    B.decode_delta_device(bt, d.mask, d.payload, d.n_c, out=bt)
+    assert np.array_equal(bt.cpu().numpy().view(np.uint16), cur)
