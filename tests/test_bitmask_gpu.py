@@ -358,3 +358,41 @@ def test_in_place_apply_sparse_record_with_a_dense_tile(dev):
     bt = _dev_u16(base, dev)
     B.decode_delta_device(bt, d.mask, d.payload, d.n_c, out=bt)
     assert np.array_equal(bt.cpu().numpy().view(np.uint16), cur)
+
+
+def test_concurrent_callers_from_threads(dev):
+    """The reference codec is pure and reentrant ("callers may encode
+    different tensors in parallel"): four host threads encode and decode
+    their own tensors through the compat API at the same time (per-thread
+    workspaces), each getting the oracle's bytes back."""
+    import threading
+    from paper_2511_12376_b200 import bitmask as B
+    from paper_2511_12376_b200.tensors import ElementType, TensorBlob
+    errors = []
+
+    def work(seed):
+        try:
+            rng = np.random.default_rng(seed)
+            for _ in range(5):
+                n = int(rng.integers(1, 300_000))
+                base = rng.integers(0, 1 << 16, n, dtype=np.uint16)
+                cur = base.copy()
+                k = int(rng.integers(0, n // 10 + 1))
+                if k:
+                    cur[rng.choice(n, k, replace=False)] ^= 1
+                tb = TensorBlob("t", ElementType.F16, (n,), base.tobytes())
+                tc = TensorBlob("t", ElementType.F16, (n,), cur.tobytes())
+                rec = B.encode_delta(tb, tc)
+                mask, payload, n_c = O.delta_encode(base, cur)
+                assert rec.changed_count == n_c and rec.packed_mask == mask.tobytes()
+                assert rec.payload == payload.tobytes()
+                assert B.decode_delta(tb, rec).data == tc.data
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(repr(e))
+
+    threads = [threading.Thread(target=work, args=(s,)) for s in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
