@@ -453,3 +453,37 @@ def test_last_unit_deeper_than_full_units(dev, monkeypatch, n, block, dist, m, e
         x = _dist(dist, n, rng).astype(np.float32)
     dq = Q.cluster_encode_device(_f32(x, dev), m, block)
     _check_units(x, m, block, dq)
+
+
+def test_concurrent_quantizer_callers_from_threads(dev):
+    """build_clusters / quantize / dequantize from three host threads at once
+    (per-thread workspaces): each thread's records equal the oracle's."""
+    import threading
+    from paper_2511_12376_b200 import quantizer as Q
+    from paper_2511_12376_b200.tensors import ElementType, TensorBlob
+    errors = []
+
+    def work(seed):
+        try:
+            rng = np.random.default_rng(seed)
+            for _ in range(4):
+                n = int(rng.integers(1, 200_000))
+                m = int(rng.integers(2, 17))
+                x = (rng.standard_normal(n) * 1e-3).astype(np.float32)
+                t = TensorBlob("t", ElementType.F32, (n,), x.tobytes())
+                table = Q.build_clusters(t, m)
+                ora = O.cluster_fit(x, m)
+                _tables_equal(table, ora)
+                q = Q.quantize(t, table)
+                packed, codes, _ = O.cluster_quantize(x, ora)
+                assert q.codes == codes.tobytes() and q.packed_labels == packed.tobytes()
+                assert Q.dequantize(q).data == O.cluster_dequantize(packed, codes, n, ora).tobytes()
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(repr(e))
+
+    threads = [threading.Thread(target=work, args=(s,)) for s in range(3)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
