@@ -275,11 +275,13 @@ def _c0_cpu_worker(args):
     names, barrier = args
     import numpy as np
     from oracle import bitsnap_oracle as O
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import bench_checkpoint as BC
     data = _C0_CPU["data"]
     model = [(n, data[n][0].shape, 0, data[n][1]) for n in names]
     prev = [(n, data[n][0].shape, 0, data[n][0]) for n in names]
     opt = [(k + n, data[n][2].shape, 1, data[n][2 + i]) for n in names
-           for i, k in enumerate(("adam.m.", "adam.v."))]
+           for i, k in enumerate((BC.M_PREFIX, BC.V_PREFIX))]
     barrier.wait()
     t0 = time.perf_counter()
     O.encode_checkpoint(model, opt, prev, "delta", 16)
@@ -528,6 +530,9 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     print(json.dumps(line), flush=True)
 
 
+C0_PUBLISHED_BLOB = 438_174_150   # 1,244,398,080 -> 438,174,150 B
+
+
 def run_c0(dev, reps: int = 3):
     """BASELINE configs[0]: a GPT-2-small checkpoint pair (bf16 weights, fp32
     Adam m/v) generated by SURVEY §8(d)'s CPU recipe — the inputs the
@@ -581,6 +586,9 @@ def run_c0(dev, reps: int = 3):
                           "blob_identical": digest == ref.get("blob_sha256"),
                           "source": "reference store.encode_checkpoint on the same inputs "
                                     "(tests/golden/make_c0_ratio.py)"},
+            "published": {"delta_blob_bytes": C0_PUBLISHED_BLOB,
+                          "reproduced": blob == C0_PUBLISHED_BLOB,
+                          "source": "BASELINE.md §2 / SURVEY §6 (2.8400x)"},
             "save_delta_gbs": round(raw / best["save_delta_s"] / 1e9, 2),
             "save_base_gbs": round(raw / best["save_base_s"] / 1e9, 2),
             "load_gbs": round(raw / best["load_s"] / 1e9, 2),
@@ -710,6 +718,7 @@ def run_ckpt_sharded(config, dev, rank, world, reps: int = 2):
     import torch
     import torch.distributed as dist
     sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import bench_checkpoint as BC
     from bench_checkpoint import generate, shapes, shard_names
     from paper_2511_12376_b200 import planner as PL
     from paper_2511_12376_b200 import store as S
@@ -726,7 +735,7 @@ def run_ckpt_sharded(config, dev, rank, world, reps: int = 2):
     for nm, _ in shp:
         specs.append(PL.TensorSpec(nm, "model", 2 * numel[nm]))
         owner.append(owner_of[nm])
-    pre = ["master.", "adam.m.", "adam.v."] if config == "C3" else ["adam.m.", "adam.v."]
+    pre = ["master.", BC.M_PREFIX, BC.V_PREFIX] if config == "C3" else [BC.M_PREFIX, BC.V_PREFIX]
     for nm, _ in shp:
         for p in pre:
             specs.append(PL.TensorSpec(p + nm, "optimizer", 4 * numel[nm]))

@@ -18,7 +18,7 @@ import torch
 
 from bitsnap import store as RS
 from bitsnap.tensors import Checkpoint, ElementType, TensorBlob
-from bench_checkpoint import shapes
+from bench_checkpoint import M_PREFIX, V_PREFIX, shapes
 
 g = torch.Generator().manual_seed(0)
 m0, m1, opt = [], [], []
@@ -31,8 +31,8 @@ for name, shp in shapes("C0"):
     b = lambda t: t.to(torch.bfloat16).view(torch.int16).numpy().astype("<i2").tobytes()
     m0.append(TensorBlob(name, ElementType.F16, tuple(shp), b(w0)))
     m1.append(TensorBlob(name, ElementType.F16, tuple(shp), b(w1)))
-    opt.append(TensorBlob("adam.m." + name, ElementType.F32, tuple(shp), m.numpy().astype("<f4").tobytes()))
-    opt.append(TensorBlob("adam.v." + name, ElementType.F32, tuple(shp), v.numpy().astype("<f4").tobytes()))
+    opt.append(TensorBlob(M_PREFIX + name, ElementType.F32, tuple(shp), m.numpy().astype("<f4").tobytes()))
+    opt.append(TensorBlob(V_PREFIX + name, ElementType.F32, tuple(shp), v.numpy().astype("<f4").tobytes()))
 c0 = Checkpoint(iteration=0, model_states=tuple(m0), optimizer_states=tuple(opt))
 c1 = Checkpoint(iteration=1, model_states=tuple(m1), optimizer_states=tuple(opt))
 t = time.time()

@@ -144,3 +144,50 @@ def test_oracle_vs_live_reference_random():
         packed, codes, _ = O.cluster_quantize(x, tab)
         assert O.quant_record("x", (n,), tab, packed, codes) == \
             quantizer.serialize_quantized(q)
+
+
+def _c0_records(names):
+    """Worker: the oracle's encode_checkpoint records of some C0 tensors
+    (model DELTA/RAW, then the two QUANT states) — concatenated in
+    checkpoint order they are the whole blob (store.py:240-247 offsets are
+    sequential)."""
+    import bench_checkpoint as BC
+    data = _C0["data"]
+    out = {}
+    for n in names:
+        w0, w1, m, v = data[n]
+        shp = w0.shape
+        _, blob_w = O.encode_checkpoint([(n, shp, 0, w1)], [], [(n, shp, 0, w0)], "delta", 16)
+        _, blob_o = O.encode_checkpoint([], [(BC.M_PREFIX + n, shp, 1, m),
+                                             (BC.V_PREFIX + n, shp, 1, v)], None, "delta", 16)
+        out[n] = (blob_w, blob_o)
+    return out
+
+
+_C0: dict = {}
+
+
+def test_c0_published_blob():
+    """BASELINE.md §2 / SURVEY §6: the reference's whole-checkpoint encode of
+    the C0 pair (SURVEY §8(d) CPU-generator recipe) is 1,244,398,080 ->
+    438,174,150 B.  The oracle reproduces that size and the reference's
+    blob digest (tests/golden/c0_ratio.json, made by make_c0_ratio.py from
+    the reference store); the GPU bench checks its blob against the same
+    digest (bench.py run_c0)."""
+    import multiprocessing as mp
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(__file__)), "tools"))
+    import bench_checkpoint as BC
+    _C0["data"] = data = BC.generate_cpu_recipe_host("C0")
+    names = list(data)
+    ncpu = max(1, min(16, len(os.sched_getaffinity(0))))
+    groups = [names[i::ncpu] for i in range(ncpu)]
+    with mp.get_context("fork").Pool(ncpu) as p:
+        parts = {}
+        for d in p.map(_c0_records, groups):
+            parts.update(d)
+    blob = b"".join(parts[n][0] for n in names) + b"".join(parts[n][1] for n in names)
+    ref = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "c0_ratio.json")))
+    raw = sum(w.nbytes + m.nbytes + v.nbytes for w, _, m, v in data.values())
+    assert raw == 1_244_398_080 == ref["raw_bytes"]
+    assert len(blob) == 438_174_150 == ref["delta_blob_bytes"]
+    assert hashlib.sha256(blob).hexdigest() == ref["blob_sha256"]

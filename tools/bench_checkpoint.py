@@ -32,19 +32,25 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
+# optimizer-state names: torch.optim.Adam's state keys as name prefixes.  With
+# the C0 tensor names below these reproduce the reference's published C0 blob
+# size exactly (438,174,150 B; record headers carry the names)
+M_PREFIX, V_PREFIX = "exp_avg.", "exp_avg_sq."
+
+
 def shapes(config: str):
     if config == "C0":
         d, ffn, vocab, ctx, layers = 768, 3072, 50257, 1024, 12
         out = [("wte", (vocab, d)), ("wpe", (ctx, d))]
         for i in range(layers):
             p = f"h.{i}."
-            out += [(p + "ln_1.w", (d,)), (p + "ln_1.b", (d,)),
-                    (p + "attn.c_attn.w", (d, 3 * d)), (p + "attn.c_attn.b", (3 * d,)),
-                    (p + "attn.c_proj.w", (d, d)), (p + "attn.c_proj.b", (d,)),
-                    (p + "ln_2.w", (d,)), (p + "ln_2.b", (d,)),
-                    (p + "mlp.c_fc.w", (d, ffn)), (p + "mlp.c_fc.b", (ffn,)),
-                    (p + "mlp.c_proj.w", (ffn, d)), (p + "mlp.c_proj.b", (d,))]
-        return out + [("ln_f.w", (d,)), ("ln_f.b", (d,))]
+            out += [(p + "ln_1.weight", (d,)), (p + "ln_1.bias", (d,)),
+                    (p + "attn.c_attn.weight", (d, 3 * d)), (p + "attn.c_attn.bias", (3 * d,)),
+                    (p + "attn.c_proj.weight", (d, d)), (p + "attn.c_proj.bias", (d,)),
+                    (p + "ln_2.weight", (d,)), (p + "ln_2.bias", (d,)),
+                    (p + "mlp.c_fc.weight", (d, ffn)), (p + "mlp.c_fc.bias", (ffn,)),
+                    (p + "mlp.c_proj.weight", (ffn, d)), (p + "mlp.c_proj.bias", (d,))]
+        return out + [("ln_f.weight", (d,)), ("ln_f.bias", (d,))]
     if config == "C3":
         d, ffn, vocab, layers = 4096, 11008, 32000, 32
         out = [("embed", (vocab, d)), ("lm_head", (vocab, d)), ("norm", (d,))]
@@ -97,9 +103,9 @@ def generate(config: str, dev, seed: int = 0, only=None):
         if config == "C3":   # BASELINE configs[3]: bf16 weights plus fp32 master, m and v
             opt.append(DeviceTensor.wrap("master." + name, w1))
         del w0, w1
-        opt.append(DeviceTensor.wrap("adam.m." + name,
+        opt.append(DeviceTensor.wrap(M_PREFIX + name,
                                      torch.randn(shp, device=dev, generator=g) * 1e-3))
-        opt.append(DeviceTensor.wrap("adam.v." + name,
+        opt.append(DeviceTensor.wrap(V_PREFIX + name,
                                      (torch.randn(shp, device=dev, generator=g) * 1e-3) ** 2))
     return (Checkpoint(iteration=0, model_states=base, optimizer_states=opt),
             Checkpoint(iteration=1, model_states=cur, optimizer_states=opt))
@@ -135,8 +141,8 @@ def generate_cpu_recipe(config: str, dev, seed: int = 0):
         bf = lambda a: torch.from_numpy(a.view("<i2")).to(dev).view(torch.bfloat16)
         base.append(DeviceTensor.wrap(name, bf(w0)))
         cur.append(DeviceTensor.wrap(name, bf(w1)))
-        opt.append(DeviceTensor.wrap("adam.m." + name, torch.from_numpy(m).to(dev)))
-        opt.append(DeviceTensor.wrap("adam.v." + name, torch.from_numpy(v).to(dev)))
+        opt.append(DeviceTensor.wrap(M_PREFIX + name, torch.from_numpy(m).to(dev)))
+        opt.append(DeviceTensor.wrap(V_PREFIX + name, torch.from_numpy(v).to(dev)))
     return (Checkpoint(iteration=0, model_states=base, optimizer_states=opt),
             Checkpoint(iteration=1, model_states=cur, optimizer_states=opt))
 
