@@ -173,6 +173,7 @@ def save_checkpoint(cfg: StoreConfig, ckpt, prev=None, encoder=None):
     app.py:62-64)."""
     S = _errors()
     kind = decide_kind(cfg, ckpt.iteration)
+    encoder_keeps = encoder is not None and bool(encoder.keep_prev)
     try:
         if encoder is None:
             encoder = S.CheckpointEncoder(clusters=cfg.quantizer_clusters, keep_prev=False)
@@ -182,9 +183,16 @@ def save_checkpoint(cfg: StoreConfig, ckpt, prev=None, encoder=None):
         manifest, out = encoder.encode(ckpt, prev, kind)
         commit(cfg, manifest, out)
     except Exception:
-        if kind == S.KIND_DELTA:
+        # the reference forces a base after a failed delta.  A resident
+        # encoder has already taken the failed checkpoint as its next delta
+        # base (or may have, mid-encode), which no committed directory holds,
+        # so a failed base save forces a base too, and the encoder forgets it:
+        # a later delta can never name an uncommitted base_iteration
+        if kind == S.KIND_DELTA or encoder_keeps:
             cfg.root.mkdir(parents=True, exist_ok=True)
             (cfg.root / NEEDS_BASE_MARKER).touch()
+        if encoder_keeps:
+            encoder.prev = None
         raise
     return manifest
 

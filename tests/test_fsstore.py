@@ -146,3 +146,33 @@ def test_save_and_load_through_store(dev, tmp_path, checkpoint_golden, golden_in
     assert (cfg.root / ".needs_base").exists()
     assert S.save_checkpoint(cfg, c1).kind == S.KIND_BASE
     assert not (cfg.root / ".needs_base").exists()
+
+
+@pytest.mark.gpu
+def test_failed_commit_with_resident_encoder(dev, tmp_path, checkpoint_golden, golden_index,
+                                             monkeypatch):
+    """A resident encoder retains each saved checkpoint as its next delta
+    base.  When the COMMIT of a base fails (disk full, ...), that base is on
+    no disk, so the next save must be a base again — not a delta naming the
+    uncommitted iteration as its base (load would hit MissingLinkError)."""
+    c0, c1 = _golden_ckpts(checkpoint_golden, golden_index["checkpoint"])
+    c2 = Checkpoint(iteration=120, model_states=c0.model_states,
+                    optimizer_states=c0.optimizer_states)
+    cfg = S.StoreConfig(tmp_path / "s", max_cached_iteration=1)   # every save a base
+    enc = S.CheckpointEncoder(dev, clusters=16)
+    assert S.save_checkpoint(cfg, c0, encoder=enc).kind == S.KIND_BASE
+
+    def boom(*a, **k):
+        raise OSError("no space left on device")
+    with monkeypatch.context() as mp:
+        mp.setattr(S, "write_tensors_bin", boom)
+        with pytest.raises(OSError):
+            S.save_checkpoint(cfg, c1, encoder=enc)       # base 110: encoded, not committed
+    assert enc.prev is None
+    assert (cfg.root / ".needs_base").exists()
+    monkeypatch.setenv("MAX_CACHED_ITERATION", "3")       # the policy would now pick a delta
+    m = S.save_checkpoint(cfg, c2, encoder=enc)
+    assert m.kind == S.KIND_BASE and m.base_iteration == 120
+    out = S.load_checkpoint(cfg)
+    assert out.iteration == 120
+    assert [t.data for t in out.model_states] == [t.data for t in c0.model_states]
