@@ -422,6 +422,22 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     # correctness of the timed configuration: decode(encode(cur)) == cur
     assert torch.equal(out, cur)
 
+    joined = None
+    if world > 1:
+        # which GPUs the ranks run on (one process per GPU): rank, device
+        # name and PCI bus id, gathered once over the job's backend
+        props = torch.cuda.get_device_properties(dev)
+        me = {"rank": rank, "local_rank": local_rank, "host": os.uname().nodename,
+              "device": props.name,
+              "pci_bus_id": f"{props.pci_domain_id:04x}:{props.pci_bus_id:02x}:"
+                            f"{props.pci_device_id:02x}"}
+        joined = [None] * world
+        dist.all_gather_object(joined, me)
+        if rank == 0:
+            # stdout carries only the JSON line; the join record goes to stderr too
+            print(f"[bench] {dist.get_backend()} process group: {world} ranks joined: "
+                  + ", ".join(f"rank {j['rank']} {j['device']} {j['pci_bus_id']}@{j['host']}"
+                              for j in joined), file=sys.stderr, flush=True)
     clocks = Clocks(local_rank)
     if world > 1:
         dist.barrier()
@@ -491,6 +507,8 @@ def run_b200(args, rank: int, world: int, local_rank: int):
         "gpu_launches": 5 * args.steps,  # encode; count, scan, offsets table, decode per step
         "clocks": clk,
     }
+    if joined:
+        line["dist"] = {"backend": dist.get_backend(), "world": world, "ranks": joined}
     if e2e:
         line["e2e"] = e2e
     if sweep:

@@ -38,6 +38,8 @@ def test_bench_two_ranks_gloo(dev):
     line = json.loads(lines[0])
     assert line["n_gpus"] == 2 and line["scaling"] == "weak"
     assert line["config"]["n_c"] > 0
+    assert line["dist"]["world"] == 2 and [r["rank"] for r in line["dist"]["ranks"]] == [0, 1]
+    assert "2 ranks joined" in out.stderr
     c = line["c0_sharded"]
     assert c["ranks"] == 2 and c["restored_bit_exact"] is True
     assert c["raw_bytes"] == 1244398080
