@@ -19,7 +19,7 @@ tables = Q.new_tables(n, block, dev)
 labels = torch.empty(Q.unit_label_bytes(n, block), dtype=torch.uint8, device=dev)
 codes = torch.empty(n, dtype=torch.uint8, device=dev)
 for _ in range(int(os.environ.get("REPS", "2"))):
-    Q.cluster_encode_async(x, 16, block, tables, labels, codes)
+    Q.cluster_encode_async(x, int(os.environ.get("M", "16")), block, tables, labels, codes)
 if os.environ.get("DEQ") == "1":  # and one dequantize of the result
     out = torch.empty_like(x)
     status = torch.zeros(4, dtype=torch.int64, device=dev)
