@@ -663,7 +663,7 @@ def run_c1_sweep(args, dev, world, reps: int = 3):
                      "(SURVEY §8(d))", "peak": hbm, "peak_kind": kind, "points": out}
 
 
-def run_c2_modes(args, dev, world, reps: int = 3):
+def run_c2_modes(args, dev, world, reps: int = 5):
     """BASELINE configs[2] in every form the bench quotes: Adam-m and Adam-v
     (v = |N(0,1e-3)|^2, one-sided, heavy-tailed), per 2^20 block and per
     tensor (the store's layout), m = 16; and the m sweep of SURVEY §8(d)
@@ -691,18 +691,26 @@ def run_c2_modes(args, dev, world, reps: int = 3):
             codes = torch.empty(n, dtype=torch.uint8, device=dev)
             res = torch.empty_like(x)
             st = rt.new_status(dev)
-            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-            te = td = 0.0
-            for r in range(reps + 1):
-                ev[0].record()
-                Q.cluster_encode_async(x, m, block, tables, labels, codes)
-                ev[1].record()
-                Q.cluster_dequantize_async(labels, codes, n, block, tables, res, st)
-                ev[2].record()
+            # each op in its own loop (a save encodes, a restore dequantizes):
+            # one untimed launch, then `reps` launches back to back between
+            # two CUDA events (steady state, no host sync between launches)
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            t = {}
+            for op in ("encode", "dequantize"):
+                def launch():
+                    if op == "encode":
+                        Q.cluster_encode_async(x, m, block, tables, labels, codes)
+                    else:
+                        Q.cluster_dequantize_async(labels, codes, n, block, tables, res, st)
+                launch()
                 torch.cuda.synchronize(dev)
-                if r:
-                    te += ev[0].elapsed_time(ev[1]) / reps
-                    td += ev[1].elapsed_time(ev[2]) / reps
+                ev[0].record()
+                for _ in range(reps):
+                    launch()
+                ev[1].record()
+                torch.cuda.synchronize(dev)
+                t[op] = ev[0].elapsed_time(ev[1]) / reps
+            te, td = t["encode"], t["dequantize"]
             (maxlab, flags), = rt.read_status(st)
             assert flags == 0 and maxlab < m
             units = Q.num_units(n, block)
