@@ -454,17 +454,74 @@ def decide(per_rank: list) -> RecoveryDecision:
     return RecoveryDecision(chosen, reports, [], trace)
 
 
-def recover(region: SlotRegion, rank: int, group=None, extra_valid=()) -> RecoveryDecision:
-    """engine.py:328-380 for one rank of a torch.distributed job: gather the
-    valid sets (this rank's verified slots plus `extra_valid`, e.g. the
-    iterations its on-disk store holds), decide, and clear this rank's slots
+def valid_iterations(region: SlotRegion, store_root, rank: int) -> set:
+    """engine.py:319-333: this rank's verified VALID / PERSISTED slots plus
+    the iterations its on-disk store holds up to the tracker's latest."""
+    from . import fsstore as F
+    valid = region_valid_iterations(region, rank)
+    cfg = rank_store(store_root, rank)
+    tracker = F.try_read_tracker(cfg)
+    if tracker is not None:
+        valid.update(it for it in F.list_iterations(cfg) if it <= tracker.latest_iteration)
+    return valid
+
+
+def gather_reports(region: SlotRegion, store_root) -> list:
+    """engine.py:309-316: the reference's simulated all-gather in one process
+    (every rank's newest valid iteration); `gather_valid` is the real one."""
+    reports = []
+    for rank in range(region.ranks):
+        valid = valid_iterations(region, store_root, rank)
+        reports.append(RankReport(rank, max(valid) if valid else None))
+    return reports
+
+
+def recover(reports: list, region: SlotRegion, store_root) -> RecoveryDecision:
+    """engine.py:344-380 (same signature, decision, pruning and trace): the
+    newest iteration every rank holds, everything newer cleared from every
+    rank's slots and pruned from its store.  ColdStartError without one."""
+    from . import fsstore as F
+    per_rank = [valid_iterations(region, store_root, r) for r in range(region.ranks)]
+    d = decide(per_rank)
+    d.reports = list(reports)
+    d.trace[0] = "all-gather reports: " + " ".join(
+        f"rank{r.rank}=" + ("none" if r.latest_valid_iteration is None
+                            else str(r.latest_valid_iteration))
+        for r in sorted(reports, key=lambda r: r.rank))
+    pruned = []
+    for rank in range(region.ranks):
+        for sl in region.slots(rank):
+            if sl.state != STATE_EMPTY and sl.iteration > d.chosen_iteration:
+                region.clear_slot(rank, sl.index)
+                pruned.append((rank, sl.iteration))
+        for it in F.prune_above(rank_store(store_root, rank), d.chosen_iteration):
+            pruned.append((rank, it))
+    d.pruned = sorted(set(pruned))
+    for rank, it in d.pruned:
+        d.trace.append(f"pruned iteration {it} on rank {rank}")
+    d.trace.append(f"recovering from iteration {d.chosen_iteration}")
+    return d
+
+
+def recover_dist(region: SlotRegion, rank: int, group=None, store_root=None,
+                 extra_valid=()) -> RecoveryDecision:
+    """`recover` for one rank of a torch.distributed job (one process per
+    GPU): gather the valid sets over the process group (`gather_valid`: this
+    rank's verified slots, its on-disk store when `store_root` is given, and
+    `extra_valid`), decide, and clear this rank's slots (and prune its store)
     newer than the chosen iteration."""
-    valid = region_valid_iterations(region, rank) | set(int(v) for v in extra_valid)
+    from . import fsstore as F
+    valid = (valid_iterations(region, store_root, rank) if store_root is not None
+             else region_valid_iterations(region, rank))
+    valid |= set(int(v) for v in extra_valid)
     d = decide(gather_valid(valid, group))
-    for s in region.slots(rank):
-        if s.state != STATE_EMPTY and s.iteration > d.chosen_iteration:
-            region.clear_slot(rank, s.index)
-            d.pruned.append((rank, s.iteration))
+    for sl in region.slots(rank):
+        if sl.state != STATE_EMPTY and sl.iteration > d.chosen_iteration:
+            region.clear_slot(rank, sl.index)
+            d.pruned.append((rank, sl.iteration))
+    if store_root is not None:
+        for it in F.prune_above(rank_store(store_root, rank), d.chosen_iteration):
+            d.pruned.append((rank, it))
     for r, it in sorted(set(d.pruned)):
         d.trace.append(f"pruned iteration {it} on rank {r}")
     d.trace.append(f"recovering from iteration {d.chosen_iteration}")

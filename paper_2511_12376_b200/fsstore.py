@@ -36,16 +36,6 @@ def _errors():
     return S
 
 
-class TrackerError(RuntimeError):
-    pass
-
-
-class MissingLinkError(RuntimeError):
-    def __init__(self, iteration: int):
-        super().__init__(f"checkpoint directory for iteration {iteration} is missing")
-        self.iteration = iteration
-
-
 @dataclass
 class StoreConfig:
     """store.py:84-111 (same fields, same MAX_CACHED_ITERATION override)."""
@@ -77,32 +67,36 @@ class StoreConfig:
         return FileLock(str(self.root / LOCK_NAME))
 
 
-def write_tracker(cfg: StoreConfig, latest: int, latest_base: int) -> None:
-    """store.py:181-187: temp file + atomic rename."""
+def write_tracker(cfg: StoreConfig, state) -> None:
+    """store.py:181-187: `state` (a store.TrackerState) through a temp file
+    and an atomic rename."""
     path = cfg.tracker_path()
     tmp = path.with_suffix(".tmp")
-    tmp.write_text(f"{latest}\n{latest_base}\n")
+    tmp.write_text(f"{state.latest_iteration}\n{state.latest_base_iteration}\n")
     os.replace(tmp, path)
 
 
-def read_tracker(cfg: StoreConfig) -> tuple:
-    """store.py:190-201 -> (latest_iteration, latest_base_iteration)."""
+def read_tracker(cfg: StoreConfig):
+    """store.py:190-201 -> store.TrackerState; TrackerError when the file is
+    missing or malformed."""
+    S = _errors()
     path = cfg.tracker_path()
     if not path.exists():
-        raise TrackerError(f"tracker file not found at {path}")
+        raise S.TrackerError(f"tracker file not found at {path}")
     lines = path.read_text().splitlines()
     if len(lines) < 2:
-        raise TrackerError(f"malformed tracker file at {path}")
+        raise S.TrackerError(f"malformed tracker file at {path}")
     try:
-        return int(lines[0]), int(lines[1])
+        latest, base = int(lines[0]), int(lines[1])
     except ValueError as exc:
-        raise TrackerError(f"malformed tracker file at {path}: {exc}") from exc
+        raise S.TrackerError(f"malformed tracker file at {path}: {exc}") from exc
+    return S.TrackerState(latest, base)
 
 
 def try_read_tracker(cfg: StoreConfig):
     try:
         return read_tracker(cfg)
-    except TrackerError:
+    except _errors().TrackerError:
         return None
 
 
@@ -128,7 +122,7 @@ def decide_kind(cfg: StoreConfig, iteration: int) -> str:
     tracker = try_read_tracker(cfg)
     if tracker is None:
         return S.KIND_BASE
-    since_base = sum(1 for it in list_iterations(cfg) if it >= tracker[1])
+    since_base = sum(1 for it in list_iterations(cfg) if it >= tracker.latest_base_iteration)
     return S.KIND_BASE if since_base >= cfg.effective_max_cached() else S.KIND_DELTA
 
 
@@ -154,8 +148,8 @@ def commit(cfg: StoreConfig, manifest, tensors) -> None:
             if manifest.kind == S.KIND_BASE:
                 base = manifest.iteration
             else:
-                base = prev[1] if prev else manifest.base_iteration
-            write_tracker(cfg, manifest.iteration, base)
+                base = prev.latest_base_iteration if prev else manifest.base_iteration
+            write_tracker(cfg, S.TrackerState(manifest.iteration, base))
             marker = cfg.root / NEEDS_BASE_MARKER
             if manifest.kind == S.KIND_BASE and marker.exists():
                 marker.unlink()
@@ -197,12 +191,39 @@ def save_checkpoint(cfg: StoreConfig, ckpt, prev=None, encoder=None):
     return manifest
 
 
+def prune_above(cfg: StoreConfig, iteration: int) -> list:
+    """store.py:533-553: remove every checkpoint newer than `iteration` (the
+    recovery consensus's disk half) and point the tracker at the newest
+    remaining one and its anchoring base.  Returns the pruned iterations."""
+    S = _errors()
+    pruned = []
+    if not cfg.root.exists():
+        return pruned
+    with cfg.lock():
+        for it in list_iterations(cfg):
+            if it > iteration:
+                shutil.rmtree(cfg.iter_dir(it), ignore_errors=True)
+                pruned.append(it)
+        remaining = list_iterations(cfg)
+        if not remaining:
+            cfg.tracker_path().unlink(missing_ok=True)
+            return pruned
+        latest = base = max(remaining)
+        while True:
+            m = read_manifest(cfg, base)
+            if m.kind == S.KIND_BASE:
+                break
+            base = m.base_iteration
+        write_tracker(cfg, S.TrackerState(latest, base))
+    return pruned
+
+
 def read_manifest(cfg: StoreConfig, iteration: int):
     """store.py:395-410."""
     S = _errors()
     d = cfg.iter_dir(iteration)
     if not d.exists():
-        raise MissingLinkError(iteration)
+        raise S.MissingLinkError(iteration)
     manifest = S.CheckpointManifest.from_bytes((d / "manifest.bin").read_bytes())
     token = (d / "type.txt").read_text().strip()
     if token != manifest.kind:
@@ -222,7 +243,7 @@ def load_checkpoint(cfg: StoreConfig, iteration: int | None = None, device=None,
     dequantized exactly as the reference's dequantize)."""
     S = _errors()
     if iteration is None:
-        iteration = read_tracker(cfg)[0]
+        iteration = read_tracker(cfg).latest_iteration
     chain, it = [], iteration
     while True:
         manifest = read_manifest(cfg, it)

@@ -58,6 +58,30 @@ class MissingPreviousError(StoreError):
     """store.py:79."""
 
 
+class TrackerError(StoreError):
+    """store.py:70."""
+
+
+class MissingLinkError(StoreError):
+    """store.py:74-77."""
+
+    def __init__(self, iteration: int):
+        super().__init__(f"checkpoint chain broken: iteration {iteration} missing")
+        self.iteration = iteration
+
+
+@dataclass(frozen=True)
+class TrackerState:
+    """store.py:114-121: the tracker file's two lines."""
+
+    latest_iteration: int
+    latest_base_iteration: int
+
+    def __post_init__(self):
+        if self.latest_base_iteration > self.latest_iteration:
+            raise TrackerError("base iteration is newer than latest iteration")
+
+
 @dataclass(frozen=True)
 class ManifestEntry:
     """store.py:124-130."""
@@ -1328,6 +1352,7 @@ def write_tensors_bin(path: str, blob) -> None:
 
 # the reference store's file-system entry points around the codec
 # (store.py:84-111, 306-474), in fsstore.py
-from .fsstore import (MissingLinkError, StoreConfig, TrackerError, commit,  # noqa: E402
-                      decide_kind, list_iterations, load_checkpoint, read_manifest,
-                      read_tracker, save_checkpoint, try_read_tracker)
+from .fsstore import (DIR_DIGITS, DIR_PREFIX, LOCK_NAME, NEEDS_BASE_MARKER,  # noqa: E402
+                      TRACKER_NAME, StoreConfig, commit, decide_kind, list_iterations,
+                      load_checkpoint, prune_above, read_manifest, read_tracker,
+                      save_checkpoint, try_read_tracker, write_tracker)

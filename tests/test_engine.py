@@ -131,17 +131,11 @@ def _consensus_region(path):
 def test_recovery_decision_matches_reference(eg, tmp_path):
     want = eg["recovery"]["consensus"]
     region = _consensus_region(tmp_path / "r1.bssl")
-    per_rank = [E.region_valid_iterations(region, r) for r in range(region.ranks)]
-    d = E.decide(per_rank)
-    # the reference's single-process recover prunes every rank's slots
-    for r in range(region.ranks):
-        for s in region.slots(r):
-            if s.state != E.STATE_EMPTY and s.iteration > d.chosen_iteration:
-                region.clear_slot(r, s.index)
-                d.pruned.append((r, s.iteration))
-    for r, it in sorted(set(d.pruned)):
-        d.trace.append(f"pruned iteration {it} on rank {r}")
-    d.trace.append(f"recovering from iteration {d.chosen_iteration}")
+    root = tmp_path / "stores"            # the ranks' on-disk stores: empty
+    # the reference's single-process entry points (engine.py:309-380)
+    reports = E.gather_reports(region, root)
+    assert [(r.rank, r.latest_valid_iteration) for r in reports] == [(0, 4), (1, 3)]
+    d = E.recover(reports, region, root)
     assert d.chosen_iteration == want["chosen"]
     assert [list(p) for p in sorted(set(d.pruned))] == want["pruned"]
     assert d.trace == want["trace"]
@@ -163,7 +157,7 @@ def _recover_worker(rank, world, port, path, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         region = E.SlotRegion.open(path)
-        d = E.recover(region, rank)
+        d = E.recover_dist(region, rank)
         q.put((rank, d.chosen_iteration, d.pruned, d.trace,
                [[x.index, x.state, x.iteration] for x in region.slots(rank)]))
         region.close()
@@ -242,3 +236,56 @@ def test_device_stage_checkpoint_matches_reference(eg, dev, checkpoint_golden, g
         info, _ = region.stage_checkpoint(0, enc, c1, c0, S.KIND_DELTA)
         m2, tb = S.unpack_blob(region.payload(0, info.index))
         assert bytes(tb) == g["blob1"].tobytes()
+
+
+def _store_recovery_setup(root, region_path, checkpoint_golden):
+    """Rank 0's store holds the golden base (100) and delta (110), rank 1's
+    only the base; rank 0 also stages 120 in memory."""
+    from paper_2511_12376_b200 import store as S
+    g = checkpoint_golden
+    links = [(S.CheckpointManifest.from_bytes(g[f"manifest{i}"].tobytes()), g[f"blob{i}"].tobytes())
+             for i in (0, 1)]
+    for rank, n in ((0, 2), (1, 1)):
+        cfg = E.rank_store(root, rank)
+        for m, b in links[:n]:
+            S.commit(cfg, m, b)
+    region = E.SlotRegion.create(region_path, ranks=2, redundancy=2, capacity=16)
+    region.stage(0, b"r0-it120", 120)
+    return region
+
+
+def test_recover_prunes_disk_like_reference(tmp_path, checkpoint_golden):
+    """engine.recover with on-disk stores (engine.py:319-380 + store.py:533-553):
+    the consensus counts each rank's committed iterations, and everything
+    newer is cleared from the slots AND pruned from the stores, the tracker
+    repaired to the newest remaining checkpoint and its base."""
+    root = tmp_path / "ours"
+    region = _store_recovery_setup(root, tmp_path / "ours.bssl", checkpoint_golden)
+    reports = E.gather_reports(region, root)
+    assert [(r.rank, r.latest_valid_iteration) for r in reports] == [(0, 120), (1, 100)]
+    d = E.recover(reports, region, root)
+    assert d.chosen_iteration == 100
+    assert d.pruned == [(0, 110), (0, 120)]
+    assert d.trace[-3:] == ["pruned iteration 110 on rank 0", "pruned iteration 120 on rank 0",
+                            "recovering from iteration 100"]
+    cfg0 = E.rank_store(root, 0)
+    assert cfg0.tracker_path().read_text() == "100\n100\n"
+    assert [p.name for p in sorted(cfg0.root.iterdir()) if p.name.startswith("iter_")] == \
+        ["iter_0000100"]
+    assert all(s.state == E.STATE_EMPTY for s in region.slots(0))
+    region.close()
+    if not os.path.isdir("/root/reference/pkg/src"):
+        return
+    # the reference's own recover on the same setup: same decision and trace
+    import sys
+    sys.path.insert(0, "/root/reference/pkg/src")
+    from bitsnap import engine as RE
+    rroot = tmp_path / "ref"
+    _store_recovery_setup(rroot, tmp_path / "ref.bssl", checkpoint_golden).close()
+    rregion = RE.SlotRegion.open(tmp_path / "ref.bssl")
+    rd = RE.recover(RE.gather_reports(rregion, rroot), rregion, rroot)
+    assert rd.chosen_iteration == d.chosen_iteration
+    assert [tuple(p) for p in rd.pruned] == d.pruned
+    assert rd.trace == d.trace
+    assert (rroot / "rank_00" / "latest_checkpointed_iteration.txt").read_text() == "100\n100\n"
+    rregion.close()

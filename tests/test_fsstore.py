@@ -61,6 +61,29 @@ def test_commit_layout_and_policy(tmp_path, checkpoint_golden, monkeypatch):
     assert S.decide_kind(cfg, 120) == S.KIND_DELTA
     with pytest.raises(S.StoreError):
         S.StoreConfig(tmp_path / "x", redundancy_depth=0)
+    # the tracker API and error types of the reference (store.py:66-121,
+    # 181-207): TrackerState, TrackerError / MissingLinkError are StoreErrors
+    assert S.read_tracker(cfg) == S.TrackerState(110, 100)
+    S.write_tracker(cfg, S.TrackerState(120, 120))
+    assert cfg.tracker_path().read_text() == "120\n120\n"
+    with pytest.raises(S.TrackerError):
+        S.TrackerState(1, 2)
+    cfg.tracker_path().write_text("garbage\n")
+    with pytest.raises(S.StoreError, match="malformed tracker"):
+        S.read_tracker(cfg)
+    assert S.try_read_tracker(cfg) is None
+    with pytest.raises(S.StoreError, match="checkpoint chain broken: iteration 105 missing"):
+        S.read_manifest(cfg, 105)
+
+
+def test_checkpoint_file_roundtrip(tmp_path, checkpoint_golden, golden_index):
+    """tensors.py:217-224: write_checkpoint_file / read_checkpoint_file."""
+    from paper_2511_12376_b200 import tensors as T
+    c0, _ = _golden_ckpts(checkpoint_golden, golden_index["checkpoint"])
+    T.write_checkpoint_file(tmp_path / "c.bsck", c0)
+    back = T.read_checkpoint_file(tmp_path / "c.bsck")
+    assert back == c0
+    assert (tmp_path / "c.bsck").read_bytes() == T.serialize_checkpoint(c0)
 
 
 @pytest.mark.skipif(not os.path.isdir(REF_SRC), reason="reference not present (GPU box)")
