@@ -36,6 +36,8 @@ from pathlib import Path
 
 import torch
 
+from . import faults
+
 REGION_MAGIC = b"BSSL"
 REGION_VERSION = 1
 REGION_HEADER = struct.Struct("<4sHIIQ")  # magic, version, ranks, K, capacity
@@ -243,8 +245,10 @@ class SlotRegion:
         return target.index
 
     def _seal(self, rank: int, idx: int, iteration: int, length: int) -> SlotInfo:
+        faults.trip("engine.stage.slot-written")
         digest = checksum(self.payload_view(rank, idx)[:length])
         self._write_header(rank, idx, STATE_VALID, iteration, length, digest)
+        faults.trip("engine.stage.slot-valid")
         return self.slot(rank, idx)
 
     def stage(self, rank: int, payload: bytes, iteration: int) -> SlotInfo:
@@ -349,6 +353,9 @@ class AsyncAgent:
                 try:
                     manifest, tensors = S.unpack_blob(self.region.payload(rank, info.index))
                     S.commit(self.rank_config(rank), manifest, tensors)
+                    faults.trip("engine.persist.committed")
+                except faults.CrashPoint:
+                    raise
                 except Exception as exc:  # keep the slot VALID for a retry
                     self.errors.append(f"rank {rank} iteration {info.iteration}: {exc}")
                     continue

@@ -24,6 +24,8 @@ from pathlib import Path
 
 from filelock import FileLock
 
+from . import faults
+
 TRACKER_NAME = "latest_checkpointed_iteration.txt"
 LOCK_NAME = ".lock"
 NEEDS_BASE_MARKER = ".needs_base"
@@ -73,7 +75,9 @@ def write_tracker(cfg: StoreConfig, state) -> None:
     path = cfg.tracker_path()
     tmp = path.with_suffix(".tmp")
     tmp.write_text(f"{state.latest_iteration}\n{state.latest_base_iteration}\n")
+    faults.trip("store.tracker.temp-written")
     os.replace(tmp, path)
+    faults.trip("store.tracker.renamed")
 
 
 def read_tracker(cfg: StoreConfig):
@@ -141,9 +145,13 @@ def commit(cfg: StoreConfig, manifest, tensors) -> None:
                 shutil.rmtree(tmp_dir)
             tmp_dir.mkdir()
             write_tensors_bin(str(tmp_dir / "tensors.bin"), tensors)
+            faults.trip("store.dir.tensors-written")
             (tmp_dir / "manifest.bin").write_bytes(manifest.to_bytes())
+            faults.trip("store.dir.manifest-written")
             (tmp_dir / "type.txt").write_text(manifest.kind + "\n")
+            faults.trip("store.dir.type-written")
             os.replace(tmp_dir, final_dir)
+            faults.trip("store.dir.renamed")
             prev = try_read_tracker(cfg)
             if manifest.kind == S.KIND_BASE:
                 base = manifest.iteration
@@ -153,6 +161,8 @@ def commit(cfg: StoreConfig, manifest, tensors) -> None:
             marker = cfg.root / NEEDS_BASE_MARKER
             if manifest.kind == S.KIND_BASE and marker.exists():
                 marker.unlink()
+        except faults.CrashPoint:
+            raise           # a crash leaves whatever it left (the tests inspect it)
         except Exception:
             shutil.rmtree(tmp_dir, ignore_errors=True)
             raise
@@ -176,6 +186,8 @@ def save_checkpoint(cfg: StoreConfig, ckpt, prev=None, encoder=None):
                                f"{cfg.quantizer_clusters}")
         manifest, out = encoder.encode(ckpt, prev, kind)
         commit(cfg, manifest, out)
+    except faults.CrashPoint:
+        raise
     except Exception:
         # the reference forces a base after a failed delta.  A resident
         # encoder has already taken the failed checkpoint as its next delta
@@ -216,6 +228,51 @@ def prune_above(cfg: StoreConfig, iteration: int) -> list:
             base = m.base_iteration
         write_tracker(cfg, S.TrackerState(latest, base))
     return pruned
+
+
+def inspect(cfg: StoreConfig) -> dict:
+    """store.py:480-503: the tracker and every checkpoint directory (kind,
+    base, record count, tensors.bin size; an unreadable one reports its
+    error)."""
+    S = _errors()
+    tracker = try_read_tracker(cfg)
+    rows = []
+    for it in list_iterations(cfg):
+        try:
+            m = read_manifest(cfg, it)
+        except S.StoreError as exc:
+            rows.append({"iteration": it, "error": str(exc)})
+            continue
+        rows.append({"iteration": it, "kind": m.kind, "base_iteration": m.base_iteration,
+                     "tensors": len(m.tensors),
+                     "tensors_bytes": (cfg.iter_dir(it) / "tensors.bin").stat().st_size})
+    return {"root": str(cfg.root),
+            "tracker": None if tracker is None else {
+                "latest_iteration": tracker.latest_iteration,
+                "latest_base_iteration": tracker.latest_base_iteration},
+            "checkpoints": rows}
+
+
+def recover_scan(cfg: StoreConfig) -> list:
+    """store.py:506-530: after a crash, delete temp debris (.tmp_* dirs, *.tmp
+    files) and every checkpoint directory newer than the tracker (never
+    committed).  Returns what it did, one line per action."""
+    done = []
+    if not cfg.root.exists():
+        return done
+    for p in list(cfg.root.iterdir()):
+        if p.name.startswith(".tmp_") or p.suffix == ".tmp":
+            if p.is_dir():
+                shutil.rmtree(p, ignore_errors=True)
+            else:
+                p.unlink(missing_ok=True)
+            done.append(f"removed temp {p.name}")
+    tracker = try_read_tracker(cfg)
+    for it in list_iterations(cfg):
+        if tracker is None or it > tracker.latest_iteration:
+            shutil.rmtree(cfg.iter_dir(it), ignore_errors=True)
+            done.append(f"pruned uncommitted iteration {it}")
+    return done
 
 
 def read_manifest(cfg: StoreConfig, iteration: int):

@@ -1353,6 +1353,7 @@ def write_tensors_bin(path: str, blob) -> None:
 # the reference store's file-system entry points around the codec
 # (store.py:84-111, 306-474), in fsstore.py
 from .fsstore import (DIR_DIGITS, DIR_PREFIX, LOCK_NAME, NEEDS_BASE_MARKER,  # noqa: E402
-                      TRACKER_NAME, StoreConfig, commit, decide_kind, list_iterations,
-                      load_checkpoint, prune_above, read_manifest, read_tracker,
-                      save_checkpoint, try_read_tracker, write_tracker)
+                      TRACKER_NAME, StoreConfig, commit, decide_kind, inspect,
+                      list_iterations, load_checkpoint, prune_above, read_manifest,
+                      read_tracker, recover_scan, save_checkpoint, try_read_tracker,
+                      write_tracker)

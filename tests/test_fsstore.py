@@ -199,3 +199,54 @@ def test_failed_commit_with_resident_encoder(dev, tmp_path, checkpoint_golden, g
     out = S.load_checkpoint(cfg)
     assert out.iteration == 120
     assert [t.data for t in out.model_states] == [t.data for t in c0.model_states]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("point", ["store.dir.tensors-written", "store.dir.manifest-written",
+                                   "store.dir.type-written", "store.dir.renamed",
+                                   "store.tracker.temp-written"])
+def test_crash_during_save_leaves_store_loadable(dev, tmp_path, checkpoint_golden, golden_index,
+                                                 point):
+    """faults.py crash points in the save pipeline (store.py:339-371,
+    181-187): a delta save crashing at any of them, then recover_scan, leaves
+    the store loading the last committed checkpoint bit for bit."""
+    from paper_2511_12376_b200 import faults
+    c0, c1 = _golden_ckpts(checkpoint_golden, golden_index["checkpoint"])
+    cfg = S.StoreConfig(tmp_path / "s", max_cached_iteration=3)
+    S.save_checkpoint(cfg, c0)
+    faults.crash_at(point)
+    try:
+        with pytest.raises(faults.CrashPoint):
+            S.save_checkpoint(cfg, c1, prev=c0)
+    finally:
+        faults.clear()
+    actions = S.recover_scan(cfg)
+    assert all(a.startswith(("removed temp", "pruned uncommitted")) for a in actions)
+    out = S.load_checkpoint(cfg)
+    assert out.iteration == 100
+    assert [t.data for t in out.model_states] == [t.data for t in c0.model_states]
+
+
+@pytest.mark.gpu
+def test_inspect_and_prune_above(dev, tmp_path, checkpoint_golden, golden_index):
+    """store.py:480-503, 533-553 over a three-link chain saved by the GPU
+    encoder: inspect lists it, prune_above removes the newest link and
+    repairs the tracker, the store then loads the middle link."""
+    c0, c1 = _golden_ckpts(checkpoint_golden, golden_index["checkpoint"])
+    c2 = Checkpoint(iteration=120, model_states=c0.model_states,
+                    optimizer_states=c0.optimizer_states)
+    cfg = S.StoreConfig(tmp_path / "s", max_cached_iteration=5)
+    enc = S.CheckpointEncoder(dev, clusters=16)
+    assert [S.save_checkpoint(cfg, c, encoder=enc).kind for c in (c0, c1, c2)] == \
+        [S.KIND_BASE, S.KIND_DELTA, S.KIND_DELTA]
+    info = S.inspect(cfg)
+    assert info["tracker"] == {"latest_iteration": 120, "latest_base_iteration": 100}
+    assert [(c["iteration"], c["kind"], c["base_iteration"]) for c in info["checkpoints"]] == \
+        [(100, "base", 100), (110, "delta", 100), (120, "delta", 110)]
+    assert all(c["tensors_bytes"] == (cfg.iter_dir(c["iteration"]) / "tensors.bin").stat().st_size
+               for c in info["checkpoints"])
+    assert S.prune_above(cfg, 110) == [120]
+    assert S.read_tracker(cfg) == S.TrackerState(110, 100)
+    out = S.load_checkpoint(cfg)
+    assert out.iteration == 110
+    assert [t.data for t in out.model_states] == [t.data for t in c1.model_states]
