@@ -1,8 +1,9 @@
 """The reference's OWN host-side test files run against this package's
 modules (INTEGRATION.md option A, CPU only): `tests/test_tensors.py` with
 `bitsnap.tensors`, `tests/test_engine.py` with `bitsnap.engine` and
-`bitsnap.faults`, and the host half of `tests/test_metrics.py` with
-`bitsnap.metrics` rebound to paper_2511_12376_b200's.  The GPU halves
+`bitsnap.faults`, the host half of `tests/test_metrics.py` with
+`bitsnap.metrics` and the tracker tests of `tests/test_store.py` with
+`bitsnap.store` rebound to paper_2511_12376_b200's.  The GPU halves
 (bitmask, quantizer, store) are restated in test_reference_suite_gpu.py:
 the reference's sources do not travel to the GPU box.  Skipped where
 /root/reference is absent."""
@@ -35,6 +36,9 @@ for _name in os.environ["BSNP_SUBST"].split(","):
     # metrics.measure runs the GPU codecs: its two end-to-end tests are the
     # GPU half (tests/test_metrics.py); the host arithmetic runs here
     ("test_metrics.py", "metrics", "not test_measure"),
+    # the store's tracker tests are host work; its save / load tests encode
+    # on the GPU (restated in tests/test_fsstore.py, test_store_gpu.py)
+    ("test_store.py", "faults,store", "tracker"),
 ])
 def test_reference_test_file_passes_on_our_module(tmp_path, test_file, subst, select):
     with open(os.path.join(REF, "tests", "conftest.py")) as f:
