@@ -38,7 +38,7 @@ for _name in os.environ["BSNP_SUBST"].split(","):
     ("test_metrics.py", "metrics", "not test_measure"),
     # the store's tracker tests are host work; its save / load tests encode
     # on the GPU (restated in tests/test_fsstore.py, test_store_gpu.py)
-    ("test_store.py", "faults,store", "tracker"),
+    ("test_store.py", "faults,store", "test_tracker or malformed_tracker or absent_tracker"),
 ])
 def test_reference_test_file_passes_on_our_module(tmp_path, test_file, subst, select):
     with open(os.path.join(REF, "tests", "conftest.py")) as f:
