@@ -187,6 +187,10 @@ def save_checkpoint(cfg: StoreConfig, ckpt, prev=None, encoder=None):
         manifest, out = encoder.encode(ckpt, prev, kind)
         commit(cfg, manifest, out)
     except faults.CrashPoint:
+        # an injected crash stands for the process dying: whatever the
+        # encoder retained may not be on disk
+        if encoder_keeps:
+            encoder.prev = None
         raise
     except Exception:
         # the reference forces a base after a failed delta.  A resident
