@@ -332,6 +332,13 @@ def cpu_baseline_c0(cores: int | None = None, max_elems: int | None = None):
                       f"numpy oracle encode_checkpoint(kind=delta); cpu: {_cpu_model()}"}
 
 
+def c1_config(n: int, p: float, world: int) -> dict:
+    """The C1 workload of the bench line — the same dict on both arms."""
+    return {"workload": "C1", "n_per_gpu": n, "p": p, "n_c": int(round(p * n)),
+            "dtype": "bf16 (raw u16 patterns)", "parallelism": f"shard x{world}",
+            "l2": "inputs 4 GiB >> 126 MB L2 (no flush needed)"}
+
+
 def run_reference(args, rank: int, world: int):
     if rank != 0:
         return
@@ -346,8 +353,9 @@ def run_reference(args, rank: int, world: int):
             "steps": args.steps, "warmup": args.warmup, "impl": "reference",
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "u16", "data": "synthetic",
-            "config": {"workload": "C1 bitmask encode+decode (bounded CPU sample)",
-                       "n": r["sample"], "p": args.p},
+            # the B200 arm's workload; each step times a bounded sample of it
+            # (cpu_baseline.sample says which)
+            "config": c1_config(1 << args.log2n, args.p, world),
             "cpu_baseline": {**r, "value": v},
             "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -490,9 +498,7 @@ def run_b200(args, rank: int, world: int, local_rank: int):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u16", "data": "synthetic",
-        "config": {"workload": "C1", "n_per_gpu": n, "p": args.p, "n_c": k,
-                   "dtype": "bf16 (raw u16 patterns)", "parallelism": f"shard x{world}",
-                   "l2": "inputs 4 GiB >> 126 MB L2 (no flush needed)"},
+        "config": c1_config(n, args.p, world),
         "ops": {"encode_gbs": round(eb / (enc_ms * 1e-3) / 1e9, 1),
                 "decode_gbs": round(db / (dec_ms * 1e-3) / 1e9, 1),
                 "encode_ms": round(enc_ms, 4), "decode_ms": round(dec_ms, 4),
