@@ -430,3 +430,27 @@ def test_07_quantizer_error_bound_and_mse():
     err = (np.frombuffer(t.data, dtype="<f4").astype(np.float64)
            - np.frombuffer(r.data, dtype="<f4").astype(np.float64))
     assert float(np.mean(err ** 2)) <= 1e-5
+
+
+# ------------------------------------------------------ empty tensors (edge)
+# BSDL bytes of the reference's encode_delta on an empty F16 tensor named "e"
+# (run here: bitmask.py:94-111 + serialize_delta :201-215): n = n_c = 0, no
+# mask, no payload
+_EMPTY_BSDL = {
+    (0,): "4253444c010000000000000000000000000000000000010065010000000000000000",
+    (3, 0): "4253444c0100000000000000000000000000000000000100650203000000000000000000000000000000",
+}
+
+
+@pytest.mark.parametrize("shape", [(0,), (3, 0)])
+def test_empty_tensor_delta(shape):
+    """An empty tensor encodes to the reference's header-only record and
+    decodes back to itself (no kernel needs to touch a byte)."""
+    a = TensorBlob("e", ElementType.F16, shape, b"")
+    rec = B.encode_delta(a, a)
+    assert rec.total_elements == 0 and rec.changed_count == 0
+    assert B.serialize_delta(rec).hex() == _EMPTY_BSDL[shape]
+    assert B.deserialize_delta(bytes.fromhex(_EMPTY_BSDL[shape])) == rec
+    out = B.decode_delta(a, rec)
+    assert out.shape == shape and out.data == b""
+    assert B.delta_size_bytes(0, 0) + 8 * (len(shape) - 1) + 1 == len(B.serialize_delta(rec))
