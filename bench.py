@@ -757,7 +757,6 @@ def run_ckpt_sharded(config, dev, rank, world, reps: int = 2):
     from paper_2511_12376_b200.tensors import ElementType
     only, lplan = shard_names(config, rank, world)
     torch.cuda.empty_cache()
-    c0, c1 = generate(config, dev, only=only)
     # specs of the WHOLE checkpoint in checkpoint order; every state of a
     # layer tensor goes to the rank the LPT plan gave the tensor
     shp = shapes(config)
@@ -777,10 +776,6 @@ def run_ckpt_sharded(config, dev, rank, world, reps: int = 2):
         load[r] += sp.nbytes
     plan = PL.ShardPlan(world=world, owner=tuple(owner), load=tuple(load))
     raw_total = sum(sp.nbytes for sp in specs)
-    enc = S.CheckpointEncoder(dev, clusters=16, keep_prev="borrow")
-    loc0 = {t.name: t for t in list(c0.model_states) + list(c0.optimizer_states)}
-    loc1 = {t.name: t for t in list(c1.model_states) + list(c1.optimizer_states)}
-    prev = {t.name: t for t in c0.model_states}
     mine = plan.local_ids(rank)
     # any encoding fits: a model state at most raw, an fp32 optimizer state
     # always quantized (1.5 B per element), plus headers (store.blob_bound)
@@ -797,17 +792,29 @@ def run_ckpt_sharded(config, dev, rank, world, reps: int = 2):
         avail = None
     local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
     need = 2 * bound * local_world
-    ok = torch.tensor([1 if (avail is None or need < 0.85 * avail) else 0], dtype=torch.int64)
+    # and this GPU's free HBM for its share: the base and current states
+    # plus the encoder's arenas and the restore (a C4 rank of 8: 103.5 GB of
+    # states, 129 GB peak, profiles/r02_dryrun_c4_rank2of8.json)
+    model_mine = sum(specs[i].nbytes for i in mine if specs[i].group == "model")
+    dev_need = int(1.3 * (plan.load[rank] + model_mine)) + (4 << 30)   # w0 and w1 both resident
+    dev_free = torch.cuda.mem_get_info(dev)[0]
+    host_ok = avail is None or need < 0.85 * avail
+    ok = torch.tensor([1 if host_ok else 0, 1 if dev_need < dev_free else 0], dtype=torch.int64)
     if world > 1:
         if dist.get_backend() == "nccl":
             ok = ok.to(dev)
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)
-    if int(ok.item()) == 0:
-        del c0, c1, loc0, loc1, prev, enc
-        torch.cuda.empty_cache()
-        return {"key": f"{config.lower()}_sharded",
-                "skipped": f"host memory: {need / 1e9:.0f} GB of landing buffers for "
-                           f"{local_world} rank(s), {(avail or 0) / 1e9:.0f} GB available"}
+    if int(ok[0].item()) == 0 or int(ok[1].item()) == 0:
+        why = (f"host memory: {need / 1e9:.0f} GB of landing buffers for {local_world} "
+               f"rank(s), {(avail or 0) / 1e9:.0f} GB available" if int(ok[0].item()) == 0 else
+               f"device memory: a rank's share needs ~{dev_need / 1e9:.0f} GB of HBM, "
+               f"{dev_free / 1e9:.0f} GB free on rank {rank}'s GPU (or another rank's)")
+        return {"key": f"{config.lower()}_sharded", "skipped": why}
+    c0, c1 = generate(config, dev, only=only)
+    enc = S.CheckpointEncoder(dev, clusters=16, keep_prev="borrow")
+    loc0 = {t.name: t for t in list(c0.model_states) + list(c0.optimizer_states)}
+    loc1 = {t.name: t for t in list(c1.model_states) + list(c1.optimizer_states)}
+    prev = {t.name: t for t in c0.model_states}
     host = [np.empty(bound, dtype=np.uint8) for _ in range(2)]
     for a in host:   # page-locked by registration (the caching allocator rounds up to 2^k)
         assert rt.lib().bsnp_host_register(a.ctypes.data, bound) == 0, "host register failed"
