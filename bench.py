@@ -510,6 +510,9 @@ def run_b200(args, rank: int, world: int, local_rank: int):
                      "algorithmic_bytes": dom_bytes,
                      "traffic": traffic["bytes"] if traffic else None,
                      "traffic_detail": traffic},
+        # the whole job's rate against N GPUs' measured HBM bandwidth
+        "box": {"gbs": round(value, 2), "gpus": world, "peak_gbs": round(world * hbm, 1),
+                "frac_of_hbm": round(value / (world * hbm), 4)},
         "gpu_launches": 5 * args.steps,  # encode; count, scan, offsets table, decode per step
         "clocks": clk,
     }
