@@ -526,6 +526,7 @@ __device__ __forceinline__ void minmax_loop(const LabelLut& L, const float* src,
 __global__ void __launch_bounds__(kQThreads)
     fit_minmax_kernel(const float* __restrict__ x, QPlan P, const float* __restrict__ fthr,
                       int* __restrict__ tile_mm, const uint32_t* __restrict__ need = nullptr) {
+  pdl_enter();
   __shared__ LabelLut L;
   __shared__ int wmin[kQThreads / 32][16], wmax[kQThreads / 32][16];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -569,6 +570,7 @@ __global__ void __launch_bounds__(kQThreads)
     fit_finalize_kernel(QPlan P, const int* __restrict__ tile_mm,
                         bsnp_cluster_table* __restrict__ tables,
                         const uint32_t* __restrict__ need = nullptr) {
+  pdl_enter();
   __shared__ int rmin[8][16], rmax[8][16];
   const uint32_t u = blockIdx.x;
   if (need && (!need[P.nunits] || !need[u])) return;
@@ -1175,47 +1177,81 @@ int var_exact_forced() {
   return e && atoi(e) != 0;
 }
 
+// launch with programmatic stream serialization: the kernel (which starts
+// with pdl_enter) is scheduled while its predecessor's last wave still runs,
+// so the chain of dependent launches does not pay a full drain + launch gap
+// per kernel; BSNP_PDL=0 launches them as ordinary kernels
+bool pdl_enabled() {
+  static const int on = [] {
+    const char* e = getenv("BSNP_PDL");
+    return !(e && atoi(e) == 0);
+  }();
+  return on != 0;
+}
+
+template <typename... KArgs, typename... Args>
+int launch_pdl(const char* what, void (*kernel)(KArgs...), dim3 grid, dim3 block,
+               cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cuda_status(what, cudaLaunchKernelEx(&cfg, kernel, ((KArgs)args)...));
+}
+
 int run_window(const float* x, const QPlan& P, bsnp_cluster_table* tables, uint8_t* labels,
                uint8_t* codes, const QWs& w, cudaStream_t s) {
   int rc;
   const unsigned tiles = (unsigned)P.total_tiles;
+  const dim3 T(kQThreads);
   // one read of x for mean and sigma (quant_stats.cuh); numpy's variance
-  // tree only for the units whose sigma interval does not decide the tables
+  // tree only for the units whose sigma interval does not decide the tables.
+  // The first kernel waits for the stream as usual; the rest follow it by
+  // programmatic dependent launch.
   fit_sum_kernel<<<tiles, kQThreads, 0, s>>>(x, P, w.partials, w.partials_q, w.list);
   if ((rc = launch_status("fit_sum_kernel"))) return rc;
-  if (P.T_max > kPreGroup) {
-    pre_combine2_kernel<<<(unsigned)(2 * P.nunits * (P.T_max >> kPreShift)), kQThreads, 0, s>>>(
-        P, w.partials, w.partials_q, w.partials2, w.partials2_q);
-    if ((rc = launch_status("pre_combine2_kernel"))) return rc;
-  }
+  if (P.T_max > kPreGroup &&
+      (rc = launch_pdl("pre_combine2_kernel", pre_combine2_kernel,
+                       dim3((unsigned)(2 * P.nunits * (P.T_max >> kPreShift))), T, s, P,
+                       w.partials, w.partials_q, w.partials2, w.partials2_q)))
+    return rc;
   // statistics + the bin grid of every unit the sigma interval decides; the
   // listed units get numpy's variance tree and their grid afterwards
-  fit_stats_kernel<<<P.nunits, kQThreads, 0, s>>>(x, P, w.partials, w.partials_q, w.partials2,
-                                                   w.partials2_q, w.mu, w.fthr, tables, w.sd,
-                                                   w.list, var_exact_forced(), w.ug,
-                                                   w.need + P.nunits);
-  if ((rc = launch_status("fit_stats_kernel"))) return rc;
-  fit_var_fallback_kernel<<<(unsigned)std::min<uint64_t>(tiles, 2 * (uint64_t)device_sms()),
-                            kQThreads, 0, s>>>(x, P, w.mu, w.list, w.partials);
-  if ((rc = launch_status("fit_var_fallback_kernel"))) return rc;
-  fit_var_combine_kernel<<<std::min(P.nunits, 256u), kQThreads, 0, s>>>(P, w.partials, w.list,
-                                                                        w.mu, w.fthr, tables,
-                                                                        w.sd, w.ug);
-  if ((rc = launch_status("fit_var_combine_kernel"))) return rc;
+  if ((rc = launch_pdl("fit_stats_kernel", fit_stats_kernel, dim3(P.nunits), T, s, x, P,
+                       w.partials, w.partials_q, w.partials2, w.partials2_q, w.mu, w.fthr,
+                       tables, w.sd, w.list, var_exact_forced(), w.ug, w.need + P.nunits)))
+    return rc;
+  if ((rc = launch_pdl("fit_var_fallback_kernel", fit_var_fallback_kernel,
+                       dim3((unsigned)std::min<uint64_t>(tiles, 2 * (uint64_t)device_sms())), T,
+                       s, x, P, w.mu, w.list, w.partials)))
+    return rc;
+  if ((rc = launch_pdl("fit_var_combine_kernel", fit_var_combine_kernel,
+                       dim3(std::min(P.nunits, 256u)), T, s, P, w.partials, w.list, w.mu, w.fthr,
+                       tables, w.sd, w.ug)))
+    return rc;
   const unsigned chunks = (unsigned)((uint64_t)(P.nunits - 1) * P.C_full + P.C_last);
-  fit_label_kernel<<<chunks, kQThreads, 0, s>>>(x, P, w.ug, labels);
-  if ((rc = launch_status("fit_label_kernel"))) return rc;
-  fit_decide_kernel<<<P.nunits, 32, 0, s>>>(P, w.ug, tables, w.need);
-  if ((rc = launch_status("fit_decide_kernel"))) return rc;
+  if ((rc = launch_pdl("fit_label_kernel", fit_label_kernel, dim3(chunks), T, s, x, P, w.ug,
+                       labels)))
+    return rc;
+  if ((rc = launch_pdl("fit_decide_kernel", fit_decide_kernel, dim3(P.nunits), dim3(32), s, P,
+                       w.ug, tables, w.need)))
+    return rc;
   // exact per-element min/max, only for the units the window left undecided
-  fit_minmax_kernel<<<std::min(tiles, 4096u), kQThreads, 0, s>>>(x, P, w.fthr, w.tile_mm,
-                                                                  w.need);
-  if ((rc = launch_status("fit_minmax_kernel"))) return rc;
-  fit_finalize_kernel<<<P.nunits, kQThreads, 0, s>>>(P, w.tile_mm, tables, w.need);
-  if ((rc = launch_status("fit_finalize_kernel"))) return rc;
+  if ((rc = launch_pdl("fit_minmax_kernel", fit_minmax_kernel, dim3(std::min(tiles, 4096u)), T,
+                       s, x, P, w.fthr, w.tile_mm, w.need)))
+    return rc;
+  if ((rc = launch_pdl("fit_finalize_kernel", fit_finalize_kernel, dim3(P.nunits), T, s, P,
+                       w.tile_mm, tables, w.need)))
+    return rc;
   if (!labels) return BSNP_OK;
-  quantize_codes_kernel<<<chunks, kQThreads, 0, s>>>(x, P, tables, labels, codes);
-  return launch_status("quantize_codes_kernel");
+  return launch_pdl("quantize_codes_kernel", quantize_codes_kernel, dim3(chunks), T, s, x, P,
+                    tables, labels, codes);
 }
 
 }  // namespace

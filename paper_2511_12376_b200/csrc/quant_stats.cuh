@@ -103,6 +103,7 @@ __device__ __forceinline__ double sum_tile_q(const float* __restrict__ x, const 
 __global__ void __launch_bounds__(kQThreads)
     fit_sum_kernel(const float* __restrict__ x, QPlan P, double* __restrict__ partials,
                    double* __restrict__ partials_q, uint32_t* __restrict__ list) {
+  pdl_enter();
   __shared__ __align__(16) float s[kSmemFloats];
   __shared__ Heap H;
   __shared__ double sw[kQThreads / 32];
@@ -122,6 +123,7 @@ __global__ void __launch_bounds__(kQThreads)
     pre_combine2_kernel(QPlan P, const double* __restrict__ partials,
                         const double* __restrict__ partials_q, double* __restrict__ partials2,
                         double* __restrict__ partials2_q) {
+  pdl_enter();
   __shared__ double v[kPreGroup];
   const uint64_t g = blockIdx.x >> 1;
   const bool isq = blockIdx.x & 1;
@@ -241,6 +243,7 @@ __global__ void __launch_bounds__(kQThreads)
                      float* __restrict__ fthr, bsnp_cluster_table* __restrict__ tables,
                      double* __restrict__ sdv, uint32_t* __restrict__ list, int force_exact,
                      UGrid* __restrict__ ug, uint32_t* __restrict__ any_need) {
+  pdl_enter();
   __shared__ double sv[kQThreads];
   __shared__ GridSmem g;
   __shared__ double s_mean, s_sd;
@@ -287,6 +290,7 @@ __global__ void __launch_bounds__(kQThreads)
 __global__ void __launch_bounds__(kQThreads)
     fit_var_fallback_kernel(const float* __restrict__ x, QPlan P, const double* __restrict__ mu,
                             const uint32_t* __restrict__ list, double* __restrict__ partials) {
+  pdl_enter();
   __shared__ __align__(16) float s[kSmemFloats];
   __shared__ Heap H;
   const uint32_t cnt = __ldcg(list);
@@ -310,6 +314,7 @@ __global__ void __launch_bounds__(kQThreads)
                            const uint32_t* __restrict__ list, const double* __restrict__ mu,
                            float* __restrict__ fthr, bsnp_cluster_table* __restrict__ tables,
                            double* __restrict__ sdv, UGrid* __restrict__ ug) {
+  pdl_enter();
   __shared__ double sv[kQThreads];
   __shared__ GridSmem g;
   __shared__ double s_sd;

@@ -393,6 +393,7 @@ __device__ __forceinline__ void label_chunk(const float* __restrict__ x, const Q
 __global__ void __launch_bounds__(kQThreads)
     fit_label_kernel(const float* __restrict__ x, QPlan P, UGrid* __restrict__ ug,
                      uint8_t* __restrict__ labels) {
+  pdl_enter();
   __shared__ __align__(16) WSmem S;
   label_chunk(x, P, chunk_of(P, blockIdx.x), ug, labels, S, policy_evict_normal());
 }
@@ -464,6 +465,7 @@ __device__ __forceinline__ bool decide_unit(const QPlan& P, uint32_t u, const UG
 __global__ void __launch_bounds__(32)
     fit_decide_kernel(QPlan P, const UGrid* __restrict__ ug,
                       bsnp_cluster_table* __restrict__ tables, uint32_t* __restrict__ need) {
+  pdl_enter();
   decide_unit(P, blockIdx.x, ug, tables, need);
 }
 
@@ -619,6 +621,7 @@ __global__ void __launch_bounds__(kQThreads)
     quantize_codes_kernel(const float* __restrict__ x, QPlan P,
                           const bsnp_cluster_table* __restrict__ tables,
                           const uint8_t* __restrict__ labels, uint8_t* __restrict__ codes) {
+  pdl_enter();
   __shared__ CodesSmem cs;
   const uint64_t nch = (uint64_t)(P.nunits - 1) * P.C_full + P.C_last;
   codes_chunk(x, P, chunk_of(P, nch - 1 - blockIdx.x), tables, labels, codes, cs,
