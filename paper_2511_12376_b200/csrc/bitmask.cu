@@ -579,6 +579,7 @@ __global__ void __launch_bounds__(kThreads)
     delta_count_kernel(const uint8_t* __restrict__ mask, uint64_t n,
                        uint32_t* __restrict__ local, uint32_t* __restrict__ ctot,
                        bsnp_status* __restrict__ st) {
+  pdl_enter();
   constexpr int kPerWarp = kChunkTiles / kWarps;
   __shared__ uint32_t s_cnt[kChunkTiles];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -631,6 +632,7 @@ __global__ void __launch_bounds__(kThreads)
 __global__ void __launch_bounds__(kThreads)
     delta_materialize_kernel(const uint64_t* __restrict__ base, const uint32_t* __restrict__ local,
                              uint64_t ntiles, uint64_t* __restrict__ off) {
+  pdl_enter();
   const uint64_t t = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
   if (t <= ntiles) off[t] = base[t >> kChunkShift] + local[t];
 }
@@ -640,6 +642,7 @@ __global__ void __launch_bounds__(kScanThreads)
                       uint64_t* __restrict__ base, uint32_t* __restrict__ local, uint64_t ntiles,
                       bsnp_status* __restrict__ st, uint64_t n_c,
                       const uint64_t* __restrict__ nc_dev) {
+  pdl_enter();
   __shared__ uint64_t s_warp[kScanThreads / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t per = (nchunks + kScanThreads - 1) / kScanThreads;
@@ -686,6 +689,7 @@ __global__ void __launch_bounds__(kThreads)
                             uint32_t* __restrict__ ticket,
                             const bsnp_status* __restrict__ st,
                             const uint64_t* __restrict__ nc_dev = nullptr) {
+  pdl_enter();
   // in place (out == base, dense chain replay): every tile is read by TMA
   // into shared memory before its words are written, tiles are disjoint, and
   // a record the validation pass rejected leaves the base untouched
@@ -839,6 +843,7 @@ __global__ void __launch_bounds__(kThreads)
                        const uint16_t* __restrict__ payload, uint64_t n, uint64_t n_c,
                        uint16_t* out, const TileOffsets offsets,
                        const bsnp_status* __restrict__ st) {
+  pdl_enter();
   __shared__ uint64_t s_warp[kWarps];
   __shared__ uint32_t s_off[kVec][kWarps];
   if (kInPlace && *(volatile const uint32_t*)&st->err_flags) return;
@@ -901,6 +906,7 @@ __global__ void __launch_bounds__(kThreads)
                             const uint16_t* __restrict__ payload, uint64_t n, uint64_t n_c,
                             uint16_t* out, const TileOffsets offsets,
                             const bsnp_status* __restrict__ st) {
+  pdl_enter();
   __shared__ __align__(16) uint16_t stage[kWarps][kApplyStage + 8];
   if (*(volatile const uint32_t*)&st->err_flags) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1186,13 +1192,13 @@ static int launch_offsets(const uint8_t* mask, uint64_t n, uint64_t n_c, const u
   delta_count_kernel<<<(unsigned)w.nchunks, kThreads, 0, s>>>(mask, n, w.local, w.ctot, status);
   int rc = launch_status("delta_count_kernel");
   if (rc) return rc;
-  delta_scan_kernel<<<1, kScanThreads, 0, s>>>(w.ctot, w.nchunks, w.base, w.local,
-                                                num_tiles(n), status, n_c, nc_dev);
-  rc = launch_status("delta_scan_kernel");
+  // the passes after the count follow it by programmatic dependent launch
+  rc = launch_pdl("delta_scan_kernel", delta_scan_kernel, dim3(1), dim3(kScanThreads), s, w.ctot,
+                  w.nchunks, w.base, w.local, num_tiles(n), status, n_c, nc_dev);
   if (rc || !materialize) return rc;
-  delta_materialize_kernel<<<(unsigned)((num_tiles(n) + kThreads) / kThreads), kThreads, 0, s>>>(
-      w.base, w.local, num_tiles(n), w.off);
-  return launch_status("delta_materialize_kernel");
+  return launch_pdl("delta_materialize_kernel", delta_materialize_kernel,
+                    dim3((unsigned)((num_tiles(n) + kThreads) / kThreads)), dim3(kThreads), s,
+                    w.base, w.local, num_tiles(n), w.off);
 }
 
 extern "C" int bsnp_delta_encode(const uint16_t* base, const uint16_t* target, uint64_t n,
@@ -1260,8 +1266,8 @@ extern "C" int bsnp_delta_decode(const uint16_t* base, const uint8_t* mask,
     const size_t smem = (size_t)kDecStages * kDecStage;
     auto k = delta_decode_tma_kernel<kDecStages, true>;
     const int grid = persistent_grid(k, smem, nt);
-    k<<<grid, kThreads, smem, s>>>(base, mask, payload, n, n_c, out, w.off, ticket2, status,
-                                   nullptr);
+    return launch_pdl_smem("delta_decode_tma_kernel", k, dim3(grid), dim3(kThreads), smem, s,
+                           base, mask, payload, n, n_c, out, w.off, ticket2, status, nullptr);
   } else if (in_place) {
     const int sms = device_sms();
     // one warp per tile, a few tiles per warp
@@ -1269,20 +1275,19 @@ extern "C" int bsnp_delta_decode(const uint16_t* base, const uint8_t* mask,
     const uint64_t want = (warps + kWarps - 1) / kWarps;
     const uint64_t cap = (uint64_t)sms * BSNP_APPLY_CTAS_PER_SM;
     const uint64_t grid = want < cap ? want : cap;
-    delta_apply_warp_kernel<<<(unsigned)(grid ? grid : 1), kThreads, 0, s>>>(
-        mask, payload, n, n_c, out, offsets, status);
+    return launch_pdl("delta_apply_warp_kernel", delta_apply_warp_kernel,
+                      dim3((unsigned)(grid ? grid : 1)), dim3(kThreads), s, mask, payload, n,
+                      n_c, out, offsets, status);
   } else if (aligned) {
     const size_t smem = (size_t)kDecStages * kDecStage;
     auto k = n_c * 32 > n ? delta_decode_tma_kernel<kDecStages, true>
                           : delta_decode_tma_kernel<kDecStages, false>;
     const int grid = persistent_grid(k, smem, nt);
-    k<<<grid, kThreads, smem, s>>>(base, mask, payload, n, n_c, out, w.off, ticket2, nullptr,
-                                   nullptr);
-  } else {
-    delta_apply_kernel<false><<<(unsigned)nt, kThreads, 0, s>>>(base, mask, payload, n, n_c,
-                                                                 out, offsets, status);
+    return launch_pdl_smem("delta_decode_tma_kernel", k, dim3(grid), dim3(kThreads), smem, s,
+                           base, mask, payload, n, n_c, out, w.off, ticket2, nullptr, nullptr);
   }
-  return launch_status("delta_decode_kernel");
+  return launch_pdl("delta_apply_kernel", delta_apply_kernel<false>, dim3((unsigned)nt),
+                    dim3(kThreads), s, base, mask, payload, n, n_c, out, offsets, status);
 }
 
 extern "C" int bsnp_delta_decode_dn(const uint16_t* base, const uint8_t* mask,
@@ -1310,9 +1315,9 @@ extern "C" int bsnp_delta_decode_dn(const uint16_t* base, const uint8_t* mask,
     const size_t smem = (size_t)kDecStages * kDecStage;
     auto k = delta_decode_tma_kernel<kDecStages, false>;
     const int grid = persistent_grid(k, smem, nt);
-    k<<<grid, kThreads, smem, s>>>(base, mask, payload, n, 0, out, w.off, ticket2, nullptr,
-                                   n_c_dev);
-    return launch_status("delta_decode_kernel");
+    return launch_pdl_smem("delta_decode_tma_kernel", k, dim3(grid), dim3(kThreads), smem, s,
+                           base, mask, payload, n, (uint64_t)0, out, w.off, ticket2, nullptr,
+                           n_c_dev);
   }
   return BSNP_E_ALIGN;
 }

@@ -1177,34 +1177,6 @@ int var_exact_forced() {
   return e && atoi(e) != 0;
 }
 
-// launch with programmatic stream serialization: the kernel (which starts
-// with pdl_enter) is scheduled while its predecessor's last wave still runs,
-// so the chain of dependent launches does not pay a full drain + launch gap
-// per kernel; BSNP_PDL=0 launches them as ordinary kernels
-bool pdl_enabled() {
-  static const int on = [] {
-    const char* e = getenv("BSNP_PDL");
-    return !(e && atoi(e) == 0);
-  }();
-  return on != 0;
-}
-
-template <typename... KArgs, typename... Args>
-int launch_pdl(const char* what, void (*kernel)(KArgs...), dim3 grid, dim3 block,
-               cudaStream_t s, Args... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  return cuda_status(what, cudaLaunchKernelEx(&cfg, kernel, ((KArgs)args)...));
-}
-
 int run_window(const float* x, const QPlan& P, bsnp_cluster_table* tables, uint8_t* labels,
                uint8_t* codes, const QWs& w, cudaStream_t s) {
   int rc;
@@ -1227,13 +1199,13 @@ int run_window(const float* x, const QPlan& P, bsnp_cluster_table* tables, uint8
                        w.partials, w.partials_q, w.partials2, w.partials2_q, w.mu, w.fthr,
                        tables, w.sd, w.list, var_exact_forced(), w.ug, w.need + P.nunits)))
     return rc;
-  if ((rc = launch_pdl("fit_var_fallback_kernel", fit_var_fallback_kernel,
-                       dim3((unsigned)std::min<uint64_t>(tiles, 2 * (uint64_t)device_sms())), T,
-                       s, x, P, w.mu, w.list, w.partials)))
+  const unsigned fb_grid = (unsigned)std::min<uint64_t>(tiles, 2 * (uint64_t)device_sms());
+  if ((rc = launch_pdl("fit_var_fallback_kernel", fit_var_fallback_kernel, dim3(fb_grid), T, s,
+                       x, P, w.mu, w.list, w.partials)))
     return rc;
   if ((rc = launch_pdl("fit_var_combine_kernel", fit_var_combine_kernel,
-                       dim3(std::min(P.nunits, 256u)), T, s, P, w.partials, w.list, w.mu, w.fthr,
-                       tables, w.sd, w.ug)))
+                       dim3(std::min(P.nunits, 256u)), T, s, P, w.partials, w.list, w.mu,
+                       w.fthr, tables, w.sd, w.ug)))
     return rc;
   const unsigned chunks = (unsigned)((uint64_t)(P.nunits - 1) * P.C_full + P.C_last);
   if ((rc = launch_pdl("fit_label_kernel", fit_label_kernel, dim3(chunks), T, s, x, P, w.ug,
