@@ -254,6 +254,7 @@ __global__ void __launch_bounds__(kEncThreads)
                            uint16_t* __restrict__ scratch, bsnp_status* __restrict__ st,
                            uint32_t* __restrict__ ticket, uint64_t* __restrict__ tile_status,
                            uint64_t ntiles, uint32_t ring_slots) {
+  pdl_enter();
   constexpr int kStages = kEncStagesWS;
   // global staging slot of record q / tile t: per tile (ring_slots == 0), or
   // a per-CTA ring of kRing slots (the workspace then does not grow with n)
@@ -1184,13 +1185,34 @@ extern "C" size_t bsnp_delta_decode_ws_bytes(uint64_t n) {
          8 * (size_t)(nt + 1);
 }
 
+// zero a status block and a workspace prefix (both 8-byte aligned, sizes in
+// u64 words) in a kernel instead of two memsets, so the codec kernel after it
+// can follow by programmatic dependent launch
+__global__ void __launch_bounds__(256)
+    zero_words_kernel(uint64_t* __restrict__ a, uint64_t na, uint64_t* __restrict__ b,
+                      uint64_t nb) {
+  pdl_enter();
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < na + nb; i += stride) {
+    if (i < na) a[i] = 0;
+    else b[i - na] = 0;
+  }
+}
+
+static int zero_prefix(bsnp_status* status, void* ws, size_t ws_bytes, cudaStream_t s) {
+  const uint64_t nb = ws_bytes / 8, nw = 2 + nb;
+  const unsigned grid = (unsigned)std::min<uint64_t>((nw + 1023) / 1024, 1024);
+  return launch_pdl("zero_words_kernel", zero_words_kernel, dim3(grid ? grid : 1), dim3(256), s,
+                    (uint64_t*)status, (uint64_t)2, (uint64_t*)ws, nb);
+}
+
 // the offsets + validation launches of a decode (n > 0)
 // materialize: also the u64 offsets array the TMA decode reads (measured:
 // its refill reading base + local directly ran 0.84 instead of 0.71 ms)
 static int launch_offsets(const uint8_t* mask, uint64_t n, uint64_t n_c, const uint64_t* nc_dev,
                           const DecWs& w, bsnp_status* status, cudaStream_t s, bool materialize) {
-  delta_count_kernel<<<(unsigned)w.nchunks, kThreads, 0, s>>>(mask, n, w.local, w.ctot, status);
-  int rc = launch_status("delta_count_kernel");
+  int rc = launch_pdl("delta_count_kernel", delta_count_kernel, dim3((unsigned)w.nchunks),
+                      dim3(kThreads), s, mask, n, w.local, w.ctot, status);
   if (rc) return rc;
   // the passes after the count follow it by programmatic dependent launch
   rc = launch_pdl("delta_scan_kernel", delta_scan_kernel, dim3(1), dim3(kScanThreads), s, w.ctot,
@@ -1212,10 +1234,12 @@ extern "C" int bsnp_delta_encode(const uint16_t* base, const uint16_t* target, u
   const size_t need = bsnp_delta_encode_ws_bytes(n);
   if (n && ws_bytes < need) return BSNP_E_WORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;
-  int rc = cuda_status("memset(status)", cudaMemsetAsync(status, 0, sizeof(bsnp_status), s));
-  if (rc || n == 0) return rc;
+  if (n == 0)
+    return cuda_status("memset(status)", cudaMemsetAsync(status, 0, sizeof(bsnp_status), s));
   const uint64_t nt = num_tiles(n);
-  rc = cuda_status("memset(ws)", cudaMemsetAsync(ws, 0, kWsHeader + 8 * nt, s));
+  // status, ticket and tile status words zeroed by a kernel the encode
+  // follows by programmatic dependent launch
+  int rc = zero_prefix(status, ws, kWsHeader + 8 * nt, s);
   if (rc) return rc;
   uint32_t* ticket = (uint32_t*)ws;
   uint64_t* tstat = (uint64_t*)((char*)ws + kWsHeader);
@@ -1227,8 +1251,9 @@ extern "C" int bsnp_delta_encode(const uint16_t* base, const uint16_t* target, u
     uint32_t ring = 0;
     enc_slots(n, &ring);
     uint16_t* scratch = (uint16_t*)((char*)ws + enc_scratch_offset(n));
-    k<<<grid, kEncThreads, smem, s>>>(base, target, n, mask, payload, payload_cap, scratch,
-                                      status, ticket, tstat, nt, ring);
+    return launch_pdl_smem("delta_encode_ws_kernel", k, dim3(grid), dim3(kEncThreads), smem, s,
+                           base, target, n, mask, payload, payload_cap, scratch, status, ticket,
+                           tstat, nt, ring);
   } else {
     delta_encode_kernel<false><<<(unsigned)nt, kThreads, 0, s>>>(
         base, target, n, mask, payload, payload_cap, status, ticket, tstat, nt);
@@ -1247,13 +1272,13 @@ extern "C" int bsnp_delta_decode(const uint16_t* base, const uint8_t* mask,
   const size_t need = bsnp_delta_decode_ws_bytes(n);
   if (n && ws_bytes < need) return BSNP_E_WORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;
-  int rc = cuda_status("memset(status)", cudaMemsetAsync(status, 0, sizeof(bsnp_status), s));
-  if (rc || n == 0) return rc;
+  if (n == 0)
+    return cuda_status("memset(status)", cudaMemsetAsync(status, 0, sizeof(bsnp_status), s));
   const uint64_t nt = num_tiles(n);
   const DecWs w = dec_ws(ws, n);
   uint32_t* ticket2 = w.ticket + 32;
   const TileOffsets offsets{w.base, w.local, nt};
-  rc = cuda_status("memset(ws)", cudaMemsetAsync(ws, 0, kWsHeader, s));
+  int rc = zero_prefix(status, ws, kWsHeader, s);
   if (rc) return rc;
   const bool in_place = (const void*)base == (const void*)out;
   const bool aligned = (((uintptr_t)base | (uintptr_t)out | (uintptr_t)mask) & 15) == 0;
@@ -1301,12 +1326,12 @@ extern "C" int bsnp_delta_decode_dn(const uint16_t* base, const uint8_t* mask,
   const size_t need = bsnp_delta_decode_ws_bytes(n);
   if (n && ws_bytes < need) return BSNP_E_WORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;
-  int rc = cuda_status("memset(status)", cudaMemsetAsync(status, 0, sizeof(bsnp_status), s));
-  if (rc || n == 0) return rc;
+  if (n == 0)
+    return cuda_status("memset(status)", cudaMemsetAsync(status, 0, sizeof(bsnp_status), s));
   const uint64_t nt = num_tiles(n);
   const DecWs w = dec_ws(ws, n);
   uint32_t* ticket2 = w.ticket + 32;
-  rc = cuda_status("memset(ws)", cudaMemsetAsync(ws, 0, kWsHeader, s));
+  int rc = zero_prefix(status, ws, kWsHeader, s);
   if (rc) return rc;
   if ((rc = launch_offsets(mask, n, 0, n_c_dev, w, status, s, true))) return rc;
   const bool aligned = (((uintptr_t)base | (uintptr_t)out | (uintptr_t)mask) & 15) == 0;
