@@ -513,7 +513,8 @@ def run_b200(args, rank: int, world: int, local_rank: int):
         # the whole job's rate against N GPUs' measured HBM bandwidth
         "box": {"gbs": round(value, 2), "gpus": world, "peak_gbs": round(world * hbm, 1),
                 "frac_of_hbm": round(value / (world * hbm), 4)},
-        "gpu_launches": 5 * args.steps,  # encode; count, scan, offsets table, decode per step
+        # per step: zero + encode; zero, count, scan, offsets table, decode
+        "gpu_launches": 7 * args.steps,
         "clocks": clk,
     }
     if joined:
