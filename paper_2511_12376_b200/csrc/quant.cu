@@ -920,10 +920,20 @@ __device__ __forceinline__ void dequant_chunk(const uint8_t* __restrict__ ls,
   }
 }
 
+// the dequantize status blocks zeroed by a kernel (not a memset node) so the
+// dequantize can follow the previous kernel by programmatic dependent launch
+__global__ void __launch_bounds__(256)
+    dq_zero_status_kernel(bsnp_status* __restrict__ st, uint32_t count) {
+  pdl_enter();
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x)
+    st[i] = bsnp_status{0, 0, 0};
+}
+
 __global__ void __launch_bounds__(kQThreads)
     dequantize_kernel(const uint8_t* __restrict__ labels, const uint8_t* __restrict__ codes,
                       QPlan P, const bsnp_cluster_table* __restrict__ tables,
                       float* __restrict__ out, bsnp_status* __restrict__ st) {
+  pdl_enter();
   __shared__ float lut[16 * 256];
   __shared__ uint32_t s_maxlab;
   // chunk -> (unit, element range)
@@ -951,6 +961,7 @@ __global__ void __launch_bounds__(kQThreads)
     dequantize_batch_kernel(const bsnp_dequant_item* __restrict__ items,
                             const uint32_t* __restrict__ first, uint32_t nitems,
                             bsnp_status* __restrict__ st) {
+  pdl_enter();
   __shared__ float lut[16 * 256];
   __shared__ uint32_t s_maxlab, s_item;
   const uint32_t b = blockIdx.x;
@@ -1304,11 +1315,12 @@ extern "C" int bsnp_cluster_dequantize(const uint8_t* labels, const uint8_t* cod
   (void)ws;
   (void)ws_bytes;
   cudaStream_t s = (cudaStream_t)stream;
-  int rc = cuda_status("memset(status)", cudaMemsetAsync(status, 0, sizeof(bsnp_status), s));
+  int rc = launch_pdl("dq_zero_status_kernel", dq_zero_status_kernel, dim3(1), dim3(256), s,
+                      status, 1u);
   if (rc) return rc;
   const uint64_t chunks = (uint64_t)(P.nunits - 1) * P.C_full + P.C_last;
-  dequantize_kernel<<<(unsigned)chunks, kQThreads, 0, s>>>(labels, codes, P, tables, out, status);
-  return launch_status("dequantize_kernel");
+  return launch_pdl("dequantize_kernel", dequantize_kernel, dim3((unsigned)chunks),
+                    dim3(kQThreads), s, labels, codes, P, tables, out, status);
 }
 
 extern "C" int bsnp_cluster_dequantize_batch(const bsnp_dequant_item* items,
